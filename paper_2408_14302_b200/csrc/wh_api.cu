@@ -1,0 +1,491 @@
+// wh_api.cu -- C ABI of libwavehop_b200: validation, plans, the on-device filter-bank
+// builder, per-clip min-max normalisation and the seam-2 kernels.
+//
+// Reference behaviour mirrored here (paths relative to /root/reference/pkg/src/wavehop):
+//   MorletParams validation   wavelet.py:47-53
+//   ScaleGrid validation      wavelet.py:62-69
+//   InvalidScale              wavelet.py:151-152
+//   InvalidHop / _check_hop   signal_io.py:153-156
+//   frames = ceil(n / hop)    wavelet.py:238
+//   half width L              wavelet.py:154
+//   taps                      wavelet.py:155-159
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <string>
+
+#include "wh_internal.h"
+
+namespace wh {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+    set_error(msg);
+    return code;
+}
+
+int64_t out_elem_bytes(const Plan &p) { return p.output == WH_OUT_COMPLEX64 ? 8 : 4; }
+
+// ---------------------------------------------------------------------------------------
+// Filter bank: fp64 sampling of the conjugated, 1/sqrt(a)-normalised Morlet exactly as
+// wavelet.py:154-159 orders it, folded (taps[L:]) and rounded to fp32.
+__global__ void k_fold_bank(const double *scales, const int64_t *half, const int64_t *off,
+                            int32_t S, double C, double Bw, float *fold, int64_t total) {
+    int32_t s = blockIdx.y;
+    if (s >= S) return;
+    double a = scales[s];
+    int64_t L = half[s];
+    double norm = pow(M_PI * Bw, -0.5);
+    double w = 2.0 * M_PI * C;
+    double rs = sqrt(a);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= L;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        double t = (double)j / a;
+        double env = norm * exp(-(t * t) / Bw);
+        double th = w * t;
+        fold[off[s] + j] = (float)((env * cos(th)) / rs);
+        fold[total + off[s] + j] = (float)((env * sin(th)) / rs);
+    }
+}
+
+int build_fold_bank(Plan &p) {
+    p.fold_off.resize(p.S);
+    int64_t tot = 0;
+    for (int s = 0; s < p.S; ++s) {
+        p.fold_off[s] = tot;
+        tot += p.half[s] + 1;
+    }
+    p.fold_total = tot;
+    WH_CUDA_TRY(cudaMalloc(&p.d_fold, sizeof(float) * 2 * tot));
+    WH_CUDA_TRY(cudaMalloc(&p.d_scales, sizeof(double) * p.S));
+    WH_CUDA_TRY(cudaMalloc(&p.d_half, sizeof(int64_t) * p.S));
+    WH_CUDA_TRY(cudaMalloc(&p.d_fold_off, sizeof(int64_t) * p.S));
+    WH_CUDA_TRY(cudaMemcpy(p.d_scales, p.scales.data(), sizeof(double) * p.S, cudaMemcpyHostToDevice));
+    WH_CUDA_TRY(cudaMemcpy(p.d_half, p.half.data(), sizeof(int64_t) * p.S, cudaMemcpyHostToDevice));
+    WH_CUDA_TRY(cudaMemcpy(p.d_fold_off, p.fold_off.data(), sizeof(int64_t) * p.S, cudaMemcpyHostToDevice));
+    dim3 grid((unsigned)std::min<int64_t>((p.Lmax + 256) / 256, 64), p.S);
+    k_fold_bank<<<grid, 256>>>(p.d_scales, p.d_half, p.d_fold_off, p.S, p.C, p.B, p.d_fold, tot);
+    WH_CUDA_TRY(cudaGetLastError());
+    WH_CUDA_TRY(cudaDeviceSynchronize());
+    return WH_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Per-clip min-max (scalogram.py:77-83 affine map, without x255/round/uint8).
+__global__ void k_minmax_reset(uint32_t *mm, int64_t clips) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < clips) {
+        mm[2 * i] = 0xffffffffu;  // min key
+        mm[2 * i + 1] = 0u;       // max key
+    }
+}
+
+__global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip, int vec) {
+    int64_t b = blockIdx.y;
+    float lo = key2f(mm[2 * b]), hi = key2f(mm[2 * b + 1]);
+    bool constant = (hi == lo);
+    float sc = constant ? 0.0f : 1.0f / (hi - lo);
+    float *base = out + b * per_clip;
+    int64_t n4 = vec ? per_clip / 4 : 0;
+    float4 *o = reinterpret_cast<float4 *>(base);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float4 v = o[i];
+        if (constant) {
+            v = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            v.x = (v.x - lo) * sc; v.y = (v.y - lo) * sc; v.z = (v.z - lo) * sc; v.w = (v.w - lo) * sc;
+        }
+        o[i] = v;
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_clip;
+         i += (int64_t)gridDim.x * blockDim.x)
+        base[i] = constant ? 0.0f : (base[i] - lo) * sc;
+}
+
+int minmax_reset(Plan &p, int64_t clips, cudaStream_t s) {
+    k_minmax_reset<<<(unsigned)((clips + 255) / 256), 256, 0, s>>>(p.d_minmax, clips);
+    WH_CUDA_TRY(cudaGetLastError());
+    return WH_OK;
+}
+
+int minmax_apply(Plan &p, int64_t clips, void *out, cudaStream_t s) {
+    int64_t per_clip = (int64_t)p.S * p.F;
+    int vec = (per_clip % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    int64_t work = vec ? per_clip / 4 : per_clip;
+    unsigned bx = (unsigned)std::min<int64_t>(std::max<int64_t>((work + 1023) / 1024, 1), 64);
+    k_minmax_apply<<<dim3(bx, (unsigned)clips), 256, 0, s>>>((float *)out, p.d_minmax, per_clip, vec);
+    WH_CUDA_TRY(cudaGetLastError());
+    return WH_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Seam 2: _kernels.py:76-91 and 93-112 on the device in float64 (one thread per frame).
+__global__ void k_strided_generic(const double *xpad, const double *tr, const double *ti,
+                                  int64_t width, int64_t hop, int64_t frames, double *ore,
+                                  double *oim) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= frames) return;
+    const double *w = xpad + k * hop;
+    double ar = 0.0, ai = 0.0;
+    for (int64_t j = 0; j < width; ++j) {
+        ar = fma(w[j], tr[j], ar);
+        ai = fma(w[j], ti[j], ai);
+    }
+    ore[k] = ar;
+    oim[k] = ai;
+}
+
+__global__ void k_strided_symmetric(const double *xpad, const double *rh, const double *ih,
+                                    int64_t half, int64_t hop, int64_t frames, double *ore,
+                                    double *oim) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= frames) return;
+    int64_t c = k * hop + half;
+    double ar = xpad[c] * rh[0], ai = 0.0;
+    for (int64_t j = 1; j <= half; ++j) {
+        double r = xpad[c + j], l = xpad[c - j];
+        ar = fma(r + l, rh[j], ar);
+        ai = fma(r - l, ih[j], ai);
+    }
+    ore[k] = ar;
+    oim[k] = ai;
+}
+
+}  // namespace wh
+
+using namespace wh;
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+extern "C" {
+
+int wh_abi_version(void) { return WH_ABI_VERSION; }
+
+const char *wh_last_error(void) { return g_last_error.c_str(); }
+
+int wh_half_width(double scale, double bandwidth, double support_radius, int64_t *half) {
+    if (!(scale > 0 && std::isfinite(scale)))
+        return fail(WH_E_INVALID_SCALE, "scale must be positive and finite");
+    if (!half) return fail(WH_E_INVALID_ARG, "half is NULL");
+    *half = (int64_t)std::ceil(support_radius * scale * std::sqrt(bandwidth / 2.0));
+    return WH_OK;
+}
+
+int wh_frame_count(int64_t n_samples, int64_t hop, int64_t *frames) {
+    if (hop < 1) return fail(WH_E_INVALID_HOP, "hop must be an integer >= 1");
+    if (n_samples < 1) return fail(WH_E_EMPTY_SIGNAL, "signal has no samples");
+    if (!frames) return fail(WH_E_INVALID_ARG, "frames is NULL");
+    *frames = (n_samples + hop - 1) / hop;
+    return WH_OK;
+}
+
+static void plan_free(Plan *p) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
+    cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
+    cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_bank); cudaFree(p->d_scale_pow);
+    cudaFree(p->d_minmax); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    cudaSetDevice(cur);
+    delete p;
+}
+
+int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_scales,
+                   double center_frequency, double bandwidth, double support_radius,
+                   int32_t wavelet, int64_t hop, int64_t n_samples, int64_t max_clips,
+                   int32_t output, int32_t norm, int32_t engine) {
+    if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+    *plan = nullptr;
+    // MorletParams (wavelet.py:47-53)
+    if (!(center_frequency > 0)) return fail(WH_E_INVALID_ARG, "center_frequency must be positive");
+    if (!(bandwidth > 0)) return fail(WH_E_INVALID_ARG, "bandwidth must be positive");
+    if (!(support_radius >= 3)) return fail(WH_E_INVALID_ARG, "support_radius must be at least 3");
+    // ScaleGrid (wavelet.py:62-69) then sample_wavelet's InvalidScale (151-152)
+    if (!scales || n_scales < 1) return fail(WH_E_INVALID_ARG, "scales must be a non-empty 1-D sequence");
+    for (int i = 0; i < n_scales; ++i)
+        if (!(scales[i] > 0 && std::isfinite(scales[i])))
+            return fail(WH_E_INVALID_SCALE, "scale must be positive and finite");
+    for (int i = 1; i < n_scales; ++i)
+        if (!(scales[i] > scales[i - 1])) return fail(WH_E_INVALID_ARG, "scales must be strictly ascending");
+    if (hop < 1) return fail(WH_E_INVALID_HOP, "hop must be an integer >= 1");
+    if (n_samples < 1) return fail(WH_E_EMPTY_SIGNAL, "signal has no samples");
+    if (max_clips < 1) return fail(WH_E_INVALID_ARG, "max_clips must be >= 1");
+    if (wavelet != WH_WAVELET_CMOR && wavelet != WH_WAVELET_RMOR)
+        return fail(WH_E_INVALID_ARG, "unknown wavelet");
+    if (output < WH_OUT_COMPLEX64 || output > WH_OUT_LOG1P) return fail(WH_E_INVALID_ARG, "unknown output");
+    if (norm != WH_NORM_NONE && norm != WH_NORM_MINMAX) return fail(WH_E_INVALID_ARG, "unknown norm");
+    if (norm == WH_NORM_MINMAX && output == WH_OUT_COMPLEX64)
+        return fail(WH_E_INVALID_ARG, "min-max normalisation needs a real output");
+    if (engine < WH_ENGINE_AUTO || engine > WH_ENGINE_UMMA) return fail(WH_E_INVALID_ARG, "unknown engine");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(WH_E_NO_DEVICE, "no CUDA device is visible");
+    if (device < 0 || device >= ndev) return fail(WH_E_NO_DEVICE, "device index out of range");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    WH_CUDA_TRY(cudaSetDevice(device));
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major != 10) {
+        cudaSetDevice(prev);
+        return fail(WH_E_UNSUPPORTED, "libwavehop_b200 is built for sm_100a (B200) only");
+    }
+
+    Plan *p = new Plan();
+    p->device = device;
+    cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+    p->S = n_scales;
+    p->scales.assign(scales, scales + n_scales);
+    p->half.resize(n_scales);
+    p->Lmax = 0;
+    for (int i = 0; i < n_scales; ++i) {
+        wh_half_width(scales[i], bandwidth, support_radius, &p->half[i]);
+        p->Lmax = std::max(p->Lmax, p->half[i]);
+    }
+    p->C = center_frequency; p->B = bandwidth; p->R = support_radius;
+    p->wavelet = wavelet; p->hop = hop; p->N = n_samples; p->F = (n_samples + hop - 1) / hop;
+    p->max_clips = max_clips; p->output = output; p->norm = norm;
+
+    int rc = build_fold_bank(*p);
+    if (rc == WH_OK && norm == WH_NORM_MINMAX) {
+        if (cudaMalloc(&p->d_minmax, sizeof(uint32_t) * 2 * max_clips) != cudaSuccess)
+            rc = fail(WH_E_OOM, "cudaMalloc(minmax) failed");
+    }
+    std::string why;
+    if (rc == WH_OK) {
+        bool umma_ok = umma_supported(*p, &why) == WH_OK;
+        if (engine == WH_ENGINE_UMMA && !umma_ok) {
+            rc = fail(WH_E_UNSUPPORTED, "UMMA engine unsupported for this plan: " + why);
+        } else {
+            p->engine = (engine == WH_ENGINE_SIMT || !umma_ok) ? WH_ENGINE_SIMT : WH_ENGINE_UMMA;
+        }
+    }
+    if (rc == WH_OK) rc = (p->engine == WH_ENGINE_UMMA) ? umma_prepare(*p) : simt_prepare(*p);
+    if (rc == WH_OK && cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
+        rc = fail(WH_E_CUDA, "cudaStreamCreate failed");
+    if (rc == WH_OK && cudaDeviceSynchronize() != cudaSuccess)
+        rc = fail(WH_E_CUDA, std::string("plan build failed: ") + cudaGetErrorString(cudaGetLastError()));
+    cudaSetDevice(prev);
+    if (rc != WH_OK) {
+        std::string msg = g_last_error;
+        plan_free(p);
+        set_error(msg);
+        return rc;
+    }
+    *plan = reinterpret_cast<wh_plan *>(p);
+    return WH_OK;
+}
+
+int wh_plan_destroy(wh_plan *plan) {
+    plan_free(reinterpret_cast<Plan *>(plan));
+    return WH_OK;
+}
+
+int wh_plan_frames(const wh_plan *plan, int64_t *frames) {
+    if (!plan || !frames) return fail(WH_E_INVALID_ARG, "NULL argument");
+    *frames = reinterpret_cast<const Plan *>(plan)->F;
+    return WH_OK;
+}
+
+int wh_plan_engine(const wh_plan *plan, int32_t *engine) {
+    if (!plan || !engine) return fail(WH_E_INVALID_ARG, "NULL argument");
+    *engine = reinterpret_cast<const Plan *>(plan)->engine;
+    return WH_OK;
+}
+
+int wh_plan_out_bytes(const wh_plan *plan, int64_t clips, int64_t *bytes) {
+    if (!plan || !bytes) return fail(WH_E_INVALID_ARG, "NULL argument");
+    const Plan *p = reinterpret_cast<const Plan *>(plan);
+    *bytes = clips * (int64_t)p->S * p->F * out_elem_bytes(*p);
+    return WH_OK;
+}
+
+int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches) {
+    if (!plan || !launches) return fail(WH_E_INVALID_ARG, "NULL argument");
+    const Plan *p = reinterpret_cast<const Plan *>(plan);
+    *launches = clips > 0 ? (1 + (p->norm == WH_NORM_MINMAX ? 2 : 0)) : 0;
+    return WH_OK;
+}
+
+int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im, int64_t cap,
+                 int64_t *half) {
+    if (!plan || !re || !im || !half) return fail(WH_E_INVALID_ARG, "NULL argument");
+    const Plan *p = reinterpret_cast<const Plan *>(plan);
+    if (scale_index < 0 || scale_index >= p->S) return fail(WH_E_INVALID_ARG, "scale index out of range");
+    int64_t L = p->half[scale_index];
+    *half = L;
+    if (cap < 2 * L + 1) return fail(WH_E_INVALID_ARG, "capacity too small");
+    std::vector<float> fr(L + 1), fi(L + 1);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    WH_CUDA_TRY(cudaSetDevice(p->device));
+    WH_CUDA_TRY(cudaMemcpy(fr.data(), p->d_fold + p->fold_off[scale_index], sizeof(float) * (L + 1),
+                           cudaMemcpyDeviceToHost));
+    WH_CUDA_TRY(cudaMemcpy(fi.data(), p->d_fold + p->fold_total + p->fold_off[scale_index],
+                           sizeof(float) * (L + 1), cudaMemcpyDeviceToHost));
+    cudaSetDevice(prev);
+    // unfold: real part even, imaginary part odd (wavelet.py:304-310 holds for Morlet taps)
+    for (int64_t j = 0; j <= L; ++j) {
+        re[L + j] = fr[j]; re[L - j] = fr[j];
+        im[L + j] = fi[j]; im[L - j] = -fi[j];
+    }
+    im[L] = fi[0];
+    return WH_OK;
+}
+
+int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev,
+               void *stream) {
+    if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (clips < 0 || clips > p->max_clips) return fail(WH_E_INVALID_ARG, "clips out of range [0, max_clips]");
+    if (clips == 0) return WH_OK;
+    if (!x_dev || !out_dev) return fail(WH_E_INVALID_ARG, "NULL buffer");
+    if (ld_x < p->N) return fail(WH_E_INVALID_ARG, "ld_x < n_samples");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != p->device) WH_CUDA_TRY(cudaSetDevice(p->device));
+    int rc = WH_OK;
+    if (p->norm == WH_NORM_MINMAX) rc = minmax_reset(*p, clips, s);
+    if (rc == WH_OK)
+        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, out_dev, s)
+                                           : simt_launch(*p, x_dev, clips, ld_x, out_dev, s);
+    if (rc == WH_OK && p->norm == WH_NORM_MINMAX) rc = minmax_apply(*p, clips, out_dev, s);
+    if (prev != p->device) cudaSetDevice(prev);
+    return rc;
+}
+
+int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out_host) {
+    if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (clips < 0 || clips > p->max_clips) return fail(WH_E_INVALID_ARG, "clips out of range [0, max_clips]");
+    if (clips == 0) return WH_OK;
+    if (!x_host || !out_host) return fail(WH_E_INVALID_ARG, "NULL buffer");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    WH_CUDA_TRY(cudaSetDevice(p->device));
+    size_t xb = sizeof(float) * (size_t)clips * p->N;
+    size_t ob = (size_t)clips * p->S * p->F * out_elem_bytes(*p);
+    if (xb > p->d_x_bytes) {
+        cudaFree(p->d_x);
+        p->d_x = nullptr;
+        size_t cap = sizeof(float) * (size_t)p->max_clips * p->N;
+        WH_CUDA_TRY(cudaMalloc(&p->d_x, cap));
+        p->d_x_bytes = cap;
+    }
+    if (ob > p->d_out_bytes) {
+        cudaFree(p->d_out);
+        p->d_out = nullptr;
+        size_t cap = (size_t)p->max_clips * p->S * p->F * out_elem_bytes(*p);
+        WH_CUDA_TRY(cudaMalloc(&p->d_out, cap));
+        p->d_out_bytes = cap;
+    }
+    WH_CUDA_TRY(cudaMemcpyAsync(p->d_x, x_host, xb, cudaMemcpyHostToDevice, p->stream));
+    int rc = wh_execute(plan, p->d_x, clips, p->N, p->d_out, p->stream);
+    if (rc != WH_OK) {
+        cudaSetDevice(prev);
+        return rc;
+    }
+    WH_CUDA_TRY(cudaMemcpyAsync(out_host, p->d_out, ob, cudaMemcpyDeviceToHost, p->stream));
+    WH_CUDA_TRY(cudaStreamSynchronize(p->stream));
+    cudaSetDevice(prev);
+    return WH_OK;
+}
+
+int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n) {
+    if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    WH_CUDA_TRY(cudaSetDevice(p->device));
+    if (!p->d_prof) {
+        WH_CUDA_TRY(cudaMalloc(&p->d_prof, sizeof(unsigned long long) * 16));
+        WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 16));
+    }
+    if (counters && n > 0) {
+        unsigned long long h[16];
+        WH_CUDA_TRY(cudaDeviceSynchronize());
+        WH_CUDA_TRY(cudaMemcpy(h, p->d_prof, sizeof h, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n && i < 16; ++i) counters[i] = h[i];
+        WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 16));
+    }
+    if (!enable) {
+        cudaFree(p->d_prof);
+        p->d_prof = nullptr;
+    }
+    cudaSetDevice(prev);
+    return WH_OK;
+}
+
+static int seam2(int device, const double *xpad, int64_t xpad_len, const double *a,
+                 const double *b, int64_t width, int64_t n_taps, int64_t hop, int64_t frames,
+                 double *ore, double *oim, bool symmetric) {
+    if (hop < 1) return fail(WH_E_INVALID_HOP, "hop must be an integer >= 1");
+    if (!xpad || !a || !b || !ore || !oim) return fail(WH_E_INVALID_ARG, "NULL buffer");
+    if (frames < 0 || width < 1) return fail(WH_E_INVALID_ARG, "bad sizes");
+    if (frames == 0) return WH_OK;
+    if (xpad_len < (frames - 1) * hop + width) return fail(WH_E_INVALID_ARG, "xpad too short");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(WH_E_NO_DEVICE, "no such CUDA device");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    WH_CUDA_TRY(cudaSetDevice(device));
+    double *dx = nullptr, *da = nullptr, *db = nullptr, *dr = nullptr, *di = nullptr;
+    size_t need = (size_t)((frames - 1) * hop + width);
+    int rc = WH_OK;
+    if (cudaMalloc(&dx, sizeof(double) * need) != cudaSuccess ||
+        cudaMalloc(&da, sizeof(double) * n_taps) != cudaSuccess ||
+        cudaMalloc(&db, sizeof(double) * n_taps) != cudaSuccess ||
+        cudaMalloc(&dr, sizeof(double) * frames) != cudaSuccess ||
+        cudaMalloc(&di, sizeof(double) * frames) != cudaSuccess) {
+        rc = fail(WH_E_OOM, "cudaMalloc failed");
+    }
+    if (rc == WH_OK) {
+        cudaMemcpy(dx, xpad, sizeof(double) * need, cudaMemcpyHostToDevice);
+        cudaMemcpy(da, a, sizeof(double) * n_taps, cudaMemcpyHostToDevice);
+        cudaMemcpy(db, b, sizeof(double) * n_taps, cudaMemcpyHostToDevice);
+        unsigned blocks = (unsigned)((frames + 127) / 128);
+        if (symmetric)
+            k_strided_symmetric<<<blocks, 128>>>(dx, da, db, n_taps - 1, hop, frames, dr, di);
+        else
+            k_strided_generic<<<blocks, 128>>>(dx, da, db, width, hop, frames, dr, di);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = fail(WH_E_CUDA, cudaGetErrorString(e));
+    }
+    if (rc == WH_OK) {
+        cudaMemcpy(ore, dr, sizeof(double) * frames, cudaMemcpyDeviceToHost);
+        cudaMemcpy(oim, di, sizeof(double) * frames, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(dx); cudaFree(da); cudaFree(db); cudaFree(dr); cudaFree(di);
+    cudaSetDevice(prev);
+    return rc;
+}
+
+int wh_strided_correlate(int device, const double *xpad, int64_t xpad_len, const double *taps_re,
+                         const double *taps_im, int64_t width, int64_t hop, int64_t frames,
+                         double *out_re, double *out_im) {
+    return seam2(device, xpad, xpad_len, taps_re, taps_im, width, width, hop, frames, out_re,
+                 out_im, false);
+}
+
+int wh_strided_correlate_symmetric(int device, const double *xpad, int64_t xpad_len,
+                                   const double *re_half, const double *im_half, int64_t half,
+                                   int64_t hop, int64_t frames, double *out_re, double *out_im) {
+    if (half < 0) return fail(WH_E_INVALID_ARG, "half < 0");
+    return seam2(device, xpad, xpad_len, re_half, im_half, 2 * half + 1, half + 1, hop, frames,
+                 out_re, out_im, true);
+}
+
+}  // extern "C"

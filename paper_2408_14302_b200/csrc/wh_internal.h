@@ -1,0 +1,153 @@
+// wh_internal.h -- shared declarations of libwavehop_b200 (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/wavehop_b200.h"
+
+namespace wh {
+
+// Thread-local last-error message behind wh_last_error().
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define WH_CUDA_TRY(expr)                                                                   \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return ::wh::fail(WH_E_CUDA, std::string(#expr " failed: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------------------
+// SIMT engine (any hop).  Folded fp32 direct correlation (the reference's
+// _kernels.py:93-112 loop, re-tiled for the GPU).
+struct SimtGroup {      // a group of <= 8 consecutive scales sharing a tap table
+    int32_t s0, ns;     // first scale, number of scales
+    int32_t L;          // max half width in the group
+    int32_t tf;         // frames per CTA tile
+    int64_t tap_off;    // offset (floats) of the group's [ns][L+1] re table (im follows)
+};
+struct SimtItem {       // one CTA of work: group g, frames [k0, k0 + tf)
+    int32_t g, k0;
+};
+
+// ---------------------------------------------------------------------------------------
+// UMMA engine (tcgen05, split-fp16).  See DESIGN.md §Kernels.
+struct UmmaPass {
+    int32_t tile_begin, tile_end;  // range in the tile table
+    int32_t s0, ns;                // scales covered by the pass
+    int32_t cols;                  // TMEM columns (multiple of 16, <= 256)
+    int32_t pad_;
+};
+struct UmmaTile {                  // one K-step (64 taps) of one pass
+    int32_t k;                     // K-step index (g in [64k, 64k+64))
+    int32_t c0;                    // first active column (multiple of 16)
+    int32_t ncols;                 // cols - c0
+    int32_t pad_;
+    int64_t byte_off;              // offset of the hi|lo tile image in the bank
+};
+
+struct Plan {
+    int device = 0;
+    int sms = 148;
+    int32_t S = 0;
+    std::vector<double> scales;
+    std::vector<int64_t> half;     // L_s (fp64 ceil, wavelet.py:154)
+    double C = 1.0, B = 1.5, R = 6.0;
+    int32_t wavelet = WH_WAVELET_CMOR;
+    int64_t hop = 1, N = 0, F = 0, max_clips = 0;
+    int32_t output = WH_OUT_COMPLEX64, norm = WH_NORM_NONE;
+    int32_t engine = WH_ENGINE_SIMT;
+    int64_t Lmax = 0;
+
+    // device filter bank: folded fp32 taps per scale (re then im), offsets per scale
+    float *d_fold = nullptr;       // [sum (L_s+1)] re, then same for im
+    std::vector<int64_t> fold_off; // host copy of per-scale offsets
+    int64_t fold_total = 0;
+    double *d_scales = nullptr;
+    int64_t *d_half = nullptr;
+    int64_t *d_fold_off = nullptr;
+
+    // SIMT engine
+    std::vector<SimtGroup> groups;
+    SimtGroup *d_groups = nullptr;
+    SimtItem *d_items = nullptr;
+    int32_t n_items = 0;
+    float *d_group_taps = nullptr; // per group [ns][L+1] re then [ns][L+1] im
+
+    // UMMA engine
+    int32_t V = 64, P = 1, Cc = 1, panels = 1;
+    int32_t Qlo = 0, G0 = 0, ksteps = 0, win_rows = 0;  // window rows (multiple of 8)
+    int32_t rows_total = 0, row_tiles = 0;
+    std::vector<UmmaPass> passes;
+    std::vector<UmmaTile> tiles;
+    UmmaPass *d_passes = nullptr;
+    UmmaTile *d_tiles = nullptr;
+    uint8_t *d_bank = nullptr;
+    int64_t bank_bytes = 0;
+    float *d_scale_pow = nullptr;  // per scale 2^-f_s
+    std::vector<int32_t> fexp;
+    int32_t bstages = 2, win_bufs = 2;
+    int32_t n_acc = 2, acc_stride = 256;   // TMEM accumulator buffers, columns per buffer
+    size_t smem_bytes = 0;     // dynamic shared memory of the engine kernel
+
+    unsigned long long *d_prof = nullptr;  // diagnostics counters (wh_plan_profile)
+
+    // per-clip min/max (ordered-uint keys) for WH_NORM_MINMAX
+    uint32_t *d_minmax = nullptr;  // [max_clips][2]
+
+    // host staging for wh_execute_host
+    float *d_x = nullptr;
+    void *d_out = nullptr;
+    size_t d_x_bytes = 0, d_out_bytes = 0;
+    cudaStream_t stream = nullptr;
+};
+
+int64_t out_elem_bytes(const Plan &p);
+
+// filter bank builders (wh_api.cu)
+int build_fold_bank(Plan &p);
+
+// engines
+int simt_prepare(Plan &p);
+int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s);
+int umma_supported(const Plan &p, std::string *why);
+int umma_prepare(Plan &p);
+int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s);
+
+// epilogue helpers (wh_api.cu)
+int minmax_reset(Plan &p, int64_t clips, cudaStream_t s);
+int minmax_apply(Plan &p, int64_t clips, void *out, cudaStream_t s);
+
+}  // namespace wh
+
+// ---- device helpers shared by the engines ----------------------------------------------
+#ifdef __CUDACC__
+namespace wh {
+// Order-preserving float <-> uint mapping for atomicMin/atomicMax on floats.
+__device__ __forceinline__ uint32_t f2key(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return __uint_as_float(u);
+}
+// scalogram.py:51-64 + BASELINE log1p, applied to the magnitude.
+__device__ __forceinline__ float apply_output(float mag, int output) {
+    switch (output) {
+        case WH_OUT_POWER: return mag * mag;
+        case WH_OUT_LOG_DB: return 20.0f * __log10f(mag + 1e-12f);
+        case WH_OUT_LOG1P: return __logf(1.0f + mag);  // abs. error ~2^-21 * |log1p|
+        default: return mag;
+    }
+}
+__device__ __forceinline__ float magnitude(float re, float im, int wavelet) {
+    return wavelet == WH_WAVELET_RMOR ? fabsf(re) : sqrtf(fmaf(re, re, im * im));
+}
+}  // namespace wh
+#endif

@@ -1,0 +1,214 @@
+// wh_simt.cu -- SIMT fp32 engine: folded direct strided correlation for any hop.
+//
+// Restates the reference's hot loop, strided_correlate_symmetric (_kernels.py:93-112):
+//   re[k] = x[c]*re0 + sum_{j=1..L} (x[c+j] + x[c-j]) * re_j,   c = k*hop (+ centring)
+//   im[k] =            sum_{j=1..L} (x[c+j] - x[c-j]) * im_j
+// with the zero padding of wavelet.py:243-246 made implicit (out-of-range samples read 0).
+//
+// Tiling: one CTA = (clip, group of <= 8 consecutive scales, tile of tf frames).  The
+// clip segment the tile touches is staged once in shared memory.  Each warp owns 4
+// frames x 8 scales; its 32 lanes split the tap index j (j = lane + 32 t), so the
+// segment reads x[c +- j] are consecutive across lanes (conflict-free for any hop) and
+// the tap reads are coalesced 128 B lines.  The 32 (or 64, complex) partial sums are
+// combined with a 31-shuffle transpose-reduction so lane l ends with output l.
+#include <algorithm>
+
+#include "wh_internal.h"
+
+namespace wh {
+
+static constexpr int SIMT_THREADS = 128;
+static constexpr int SIMT_G = 8;            // scales per group
+static constexpr int SIMT_SEG_MAX = 48 * 1024;  // floats of staged segment (192 KB)
+
+__global__ void k_group_taps(const float *fold, const int64_t *fold_off, const int64_t *half,
+                             int64_t fold_total, const SimtGroup *groups, int32_t n_groups,
+                             float *gt) {
+    int32_t g = blockIdx.y;
+    if (g >= n_groups) return;
+    SimtGroup G = groups[g];
+    int64_t width = G.L + 1;
+    int64_t n = (int64_t)G.ns * width;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int s = (int)(i / width);
+        int64_t j = i % width;
+        int sg = G.s0 + s;
+        bool in = j <= half[sg];
+        gt[G.tap_off + i] = in ? fold[fold_off[sg] + j] : 0.0f;
+        gt[G.tap_off + n + i] = in ? fold[fold_total + fold_off[sg] + j] : 0.0f;
+    }
+}
+
+// 32 values per lane -> lane l holds sum over lanes of v[l] (31 shuffles).
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+    for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+        bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            float send = upper ? v[i] : v[i + n / 2];
+            float keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(SIMT_THREADS)
+k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_t F,
+       const SimtGroup *__restrict__ groups, const SimtItem *__restrict__ items,
+       const float *__restrict__ gtaps, int32_t S, int32_t wavelet, int32_t output,
+       void *__restrict__ out, uint32_t *__restrict__ minmax) {
+    extern __shared__ float xs[];
+    const int64_t b = blockIdx.x;
+    const SimtItem it = items[blockIdx.y];
+    const SimtGroup G = groups[it.g];
+    const int L = G.L;
+    const int64_t k0 = it.k0;
+    const int nf = (int)(F - k0 < (int64_t)G.tf ? F - k0 : (int64_t)G.tf);
+    const int64_t seg_start = k0 * hop - L;
+    const int64_t seg_len = (int64_t)(nf - 1) * hop + 2 * L + 1;
+    const float *xb = x + b * ld_x;
+    for (int64_t i = threadIdx.x; i < seg_len; i += SIMT_THREADS) {
+        int64_t g = seg_start + i;
+        xs[i] = (g >= 0 && g < N) ? __ldg(xb + g) : 0.0f;
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int width = L + 1;
+    const float *tre = gtaps + G.tap_off;
+    const float *tim = tre + (int64_t)G.ns * width;
+    float lmin = INFINITY, lmax = -INFINITY;
+
+    for (int fq = warp * 4; fq < nf; fq += 4 * (SIMT_THREADS / 32)) {
+        float ar[32], ai[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            ar[i] = 0.0f;
+            ai[i] = 0.0f;
+        }
+        int c[4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) c[f] = min(fq + f, nf - 1) * (int)hop + L;
+        for (int j = lane; j <= L; j += 32) {
+            float p[4], d[4];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                float xp = xs[c[f] + j], xm = xs[c[f] - j];
+                p[f] = (j == 0) ? xp : xp + xm;
+                d[f] = xp - xm;
+            }
+#pragma unroll
+            for (int s = 0; s < SIMT_G; ++s) {
+                if (s < G.ns) {
+                    float tr = __ldg(tre + s * width + j);
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) ar[f * 8 + s] = fmaf(p[f], tr, ar[f * 8 + s]);
+                    if constexpr (CPLX) {
+                        float ti = __ldg(tim + s * width + j);
+#pragma unroll
+                        for (int f = 0; f < 4; ++f) ai[f * 8 + s] = fmaf(d[f], ti, ai[f * 8 + s]);
+                    }
+                }
+            }
+        }
+        float re = transpose_reduce32(ar, lane);
+        float im = 0.0f;
+        if constexpr (CPLX) im = transpose_reduce32(ai, lane);
+        const int f = lane >> 3, s = lane & 7;
+        const int64_t k = k0 + fq + f;
+        if (s < G.ns && fq + f < nf) {
+            const int64_t o = (b * S + G.s0 + s) * F + k;
+            if (output == WH_OUT_COMPLEX64) {
+                reinterpret_cast<float2 *>(out)[o] =
+                    make_float2(re, wavelet == WH_WAVELET_RMOR ? 0.0f : im);
+            } else {
+                float v = apply_output(magnitude(re, im, wavelet), output);
+                reinterpret_cast<float *>(out)[o] = v;
+                lmin = fminf(lmin, v);
+                lmax = fmaxf(lmax, v);
+            }
+        }
+    }
+    if (minmax) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
+            lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
+        }
+        if (lane == 0 && lmin <= lmax) {
+            atomicMin(minmax + 2 * b, f2key(lmin));
+            atomicMax(minmax + 2 * b + 1, f2key(lmax));
+        }
+    }
+}
+
+int simt_prepare(Plan &p) {
+    // groups of SIMT_G consecutive scales, heaviest (largest L) first
+    p.groups.clear();
+    int64_t tap_off = 0;
+    for (int s0 = 0; s0 < p.S; s0 += SIMT_G) {
+        SimtGroup G{};
+        G.s0 = s0;
+        G.ns = std::min(SIMT_G, p.S - s0);
+        int64_t L = 0;
+        for (int s = s0; s < s0 + G.ns; ++s) L = std::max(L, p.half[s]);
+        if (2 * L + 1 > SIMT_SEG_MAX)
+            return fail(WH_E_UNSUPPORTED, "scale too large for the SIMT engine's staged segment");
+        G.L = (int32_t)L;
+        int64_t tf = (SIMT_SEG_MAX - 2 * L - 1) / p.hop + 1;
+        tf = std::min<int64_t>(tf, 128);
+        if (tf >= 16) tf = tf / 16 * 16;
+        tf = std::max<int64_t>(1, std::min<int64_t>(tf, p.F));
+        G.tf = (int32_t)tf;
+        G.tap_off = tap_off;
+        tap_off += 2 * (int64_t)G.ns * (L + 1);
+        p.groups.push_back(G);
+    }
+    std::vector<int> order(p.groups.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return p.groups[a].L > p.groups[b].L; });
+    std::vector<SimtItem> items;
+    for (int g : order)
+        for (int64_t k0 = 0; k0 < p.F; k0 += p.groups[g].tf) items.push_back(SimtItem{g, (int32_t)k0});
+    if (items.size() > 65535u) return fail(WH_E_UNSUPPORTED, "too many SIMT work items");
+    p.n_items = (int32_t)items.size();
+    WH_CUDA_TRY(cudaMalloc(&p.d_groups, sizeof(SimtGroup) * p.groups.size()));
+    WH_CUDA_TRY(cudaMalloc(&p.d_items, sizeof(SimtItem) * items.size()));
+    WH_CUDA_TRY(cudaMalloc(&p.d_group_taps, sizeof(float) * std::max<int64_t>(tap_off, 1)));
+    WH_CUDA_TRY(cudaMemcpy(p.d_groups, p.groups.data(), sizeof(SimtGroup) * p.groups.size(),
+                           cudaMemcpyHostToDevice));
+    WH_CUDA_TRY(cudaMemcpy(p.d_items, items.data(), sizeof(SimtItem) * items.size(), cudaMemcpyHostToDevice));
+    dim3 grid(64, (unsigned)p.groups.size());
+    k_group_taps<<<grid, 256>>>(p.d_fold, p.d_fold_off, p.d_half, p.fold_total, p.d_groups,
+                                (int32_t)p.groups.size(), p.d_group_taps);
+    WH_CUDA_TRY(cudaGetLastError());
+    size_t smem = 0;
+    for (auto &G : p.groups)
+        smem = std::max<size_t>(smem, sizeof(float) * ((int64_t)(G.tf - 1) * p.hop + 2 * G.L + 1));
+    p.smem_bytes = smem;
+    WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return WH_OK;
+}
+
+int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s) {
+    if (clips > 2147483647LL) return fail(WH_E_INVALID_ARG, "too many clips");
+    dim3 grid((unsigned)clips, (unsigned)p.n_items);
+    bool cplx = p.wavelet == WH_WAVELET_CMOR;
+    uint32_t *mm = p.norm == WH_NORM_MINMAX ? p.d_minmax : nullptr;
+    if (cplx)
+        k_simt<true><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
+                                                             p.d_group_taps, p.S, p.wavelet, p.output, out, mm);
+    else
+        k_simt<false><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
+                                                              p.d_group_taps, p.S, p.wavelet, p.output, out, mm);
+    WH_CUDA_TRY(cudaGetLastError());
+    return WH_OK;
+}
+
+}  // namespace wh
