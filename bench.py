@@ -220,9 +220,11 @@ def run_ours(args, w):
         per_rank = args.clips or w["clips"]
         start = rank * per_rank
     else:
+        from paper_2408_14302_b200.shard import shard_range
+
         total = args.clips or w["clips"]
-        per_rank = total // world
-        start = rank * per_rank
+        start, stop = shard_range(total, world, rank)
+        per_rank = stop - start
     xh = make_inputs(w, per_rank, start)
     params = wh.MorletParams()
     plan = wh.CwthPlan(w["scales"], params, w["hop"], w["n"], wavelet=w["wavelet"],
@@ -288,7 +290,7 @@ def run_ours(args, w):
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     dev_ms, e2e_ms_max = float(vals[0]), float(vals[1])
-    total_clips = per_rank * world
+    total_clips = per_rank * world if w["scaling"] == "weak" else (args.clips or w["clips"])
     value = coeffs(w, total_clips) * args.steps / (dev_ms / 1e3)
     result = None
     if rank == 0:

@@ -27,6 +27,7 @@ static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
 int fail(int code, const std::string &msg) {
     set_error(msg);
+    (void)cudaGetLastError();  // do not leak a non-sticky CUDA error into later calls
     return code;
 }
 
@@ -264,14 +265,22 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
     }
     std::string why;
     if (rc == WH_OK) {
-        bool umma_ok = umma_supported(*p, &why) == WH_OK;
+        const bool umma_ok = umma_supported(*p, &why) == WH_OK;
         if (engine == WH_ENGINE_UMMA && !umma_ok) {
             rc = fail(WH_E_UNSUPPORTED, "UMMA engine unsupported for this plan: " + why);
+        } else if (engine == WH_ENGINE_SIMT || !umma_ok) {
+            p->engine = WH_ENGINE_SIMT;
+            rc = simt_prepare(*p);
         } else {
-            p->engine = (engine == WH_ENGINE_SIMT || !umma_ok) ? WH_ENGINE_SIMT : WH_ENGINE_UMMA;
+            p->engine = WH_ENGINE_UMMA;
+            rc = umma_prepare(*p);
+            if (rc == WH_E_UNSUPPORTED && engine == WH_ENGINE_AUTO) {
+                // the tensor-core planner could not fit this plan: SIMT handles any plan
+                p->engine = WH_ENGINE_SIMT;
+                rc = simt_prepare(*p);
+            }
         }
     }
-    if (rc == WH_OK) rc = (p->engine == WH_ENGINE_UMMA) ? umma_prepare(*p) : simt_prepare(*p);
     if (rc == WH_OK && cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
         rc = fail(WH_E_CUDA, "cudaStreamCreate failed");
     if (rc == WH_OK && cudaDeviceSynchronize() != cudaSuccess)

@@ -93,6 +93,7 @@ struct Plan {
     std::vector<int32_t> fexp;
     int32_t bstages = 2, win_bufs = 2;
     int32_t n_acc = 2, acc_stride = 256;   // TMEM accumulator buffers, columns per buffer
+    int32_t use_stg = 1;                   // fp32 window staged by cp.async.bulk
     size_t smem_bytes = 0;     // dynamic shared memory of the engine kernel
 
     unsigned long long *d_prof = nullptr;  // diagnostics counters (wh_plan_profile)

@@ -201,6 +201,7 @@ int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     dim3 grid((unsigned)clips, (unsigned)p.n_items);
     bool cplx = p.wavelet == WH_WAVELET_CMOR;
     uint32_t *mm = p.norm == WH_NORM_MINMAX ? p.d_minmax : nullptr;
+    (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     if (cplx)
         k_simt<true><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
                                                              p.d_group_taps, p.S, p.wavelet, p.output, out, mm);

@@ -45,6 +45,7 @@ struct UmmaArgs {
     int32_t row_tiles, V, P, Cc, panels, Qlo, win_rows, S;
     int32_t n_passes, n_tiles, wavelet, output, bstages, win_bufs, vec_ok;
     int32_t n_acc, acc_stride;          // accumulator buffers; columns per buffer (main|corr)
+    int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
     const UmmaPass *passes;
     const UmmaTile *tiles;
     const uint8_t *bank;
@@ -313,7 +314,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     uint8_t *stage_base = smem + (size_t)A.win_bufs * 2 * WH;
     const uint32_t panel_bytes = (uint32_t)A.win_rows * 128u;
     // pass / tile tables (compact) after the fp32 staging buffer
-    int4 *s_pass = reinterpret_cast<int4 *>(stage_base + (size_t)A.bstages * A.stage_bytes + 2 * (size_t)WH);
+    int4 *s_pass = reinterpret_cast<int4 *>(stage_base + (size_t)A.bstages * A.stage_bytes +
+                                            (A.use_stg ? 2 * (size_t)WH : 0));
     uint2 *s_tile = reinterpret_cast<uint2 *>(s_pass + A.n_passes);
     for (int i = threadIdx.x; i < A.n_passes; i += blockDim.x) {
         const UmmaPass ps = A.passes[i];
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
             lo = w0 > 0 ? w0 : 0;
             hi = w0 + wlen < A.N ? w0 + wlen : (A.N & ~(int64_t)3);
-            if (!A.vec_ok || hi <= lo) { lo = hi = w0; }
+            if (!A.vec_ok || !A.use_stg || hi <= lo) { lo = hi = w0; }
             (void)b;
         };
         auto issue = [&](int64_t item) {
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
-        if (ct == 0 && (int64_t)blockIdx.x < A.items) issue(blockIdx.x);
+        if (A.use_stg && ct == 0 && (int64_t)blockIdx.x < A.items) issue(blockIdx.x);
         uint32_t wcnt = 0;
         for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x, ++wcnt) {
             const int64_t b = item / A.row_tiles;
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             const uint32_t wb = wcnt % A.win_bufs;
             int64_t slo, shi;
             staged(item, slo, shi);
-            mbar_wait_p(&stg_full, wcnt & 1, pa, 0, pon);
+            if (A.use_stg) mbar_wait_p(&stg_full, wcnt & 1, pa, 0, pon);
             // sample g of the window (clip index w0 + g): staged, direct (edge), or zero
             auto load8 = [&](int row, int panel, int c8, float (&v)[8]) {
                 const int64_t off = (int64_t)row * A.V + panel * 64 + c8 * 8;
@@ -484,6 +486,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 if (g0 >= slo && g0 + 8 <= shi) {
                     const float4 u = *reinterpret_cast<const float4 *>(stg + off);
                     const float4 w = *reinterpret_cast<const float4 *>(stg + off + 4);
+                    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
+                } else if (A.vec_ok && g0 >= 0 && g0 + 8 <= A.N) {
+                    const float4 u = __ldg(reinterpret_cast<const float4 *>(xb + g0));
+                    const float4 w = __ldg(reinterpret_cast<const float4 *>(xb + g0) + 1);
                     v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
                 } else {
 #pragma unroll
@@ -495,6 +501,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             };
             // pass 1: max |x| over the window
             float mx = 0.0f;
+#pragma unroll 4
             for (int c = ct; c < chunks; c += UM_CONV_THREADS) {
                 const int row = c / (A.panels * 8), rem = c % (A.panels * 8);
                 float v[8];
@@ -543,7 +550,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             if (ct == 0) wexp[wb] = ldexpf(1.0f, -ex);
             asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
             // staging is free again: prefetch the next item's window
-            if (ct == 0 && item + gridDim.x < A.items) issue(item + gridDim.x);
+            if (A.use_stg && ct == 0 && item + gridDim.x < A.items) issue(item + gridDim.x);
             if (lane == 0) mbar_arrive(&win_full[wb]);
         }
     } else {
@@ -738,8 +745,9 @@ int umma_supported(const Plan &p, std::string *why) {
     const int64_t qmax = (ksteps - 1) * 64 / V;
     const int64_t rows = ((128 + qmax) + 7) / 8 * 8;
     const int64_t win = 2 * (V / 64) * rows * 128;
-    // smallest configuration: one window + its fp32 staging, two 128-column stages
-    if (2 * win + 2 * 128 * 384 > UM_SMEM_BUDGET) {
+    // smallest configuration: one window (no staging), two 16-column stages (the planner
+    // makes the final decision with the real stage size)
+    if (win + 2 * 16 * 384 > UM_SMEM_BUDGET) {
         if (why) *why = "tap support too long for a resident shared-memory window";
         return WH_E_UNSUPPORTED;
     }
@@ -843,19 +851,26 @@ int umma_prepare(Plan &p) {
     const int64_t table_bytes = 16 * (int64_t)p.passes.size() + 8 * (int64_t)p.tiles.size();
     const int64_t budget = UM_SMEM_BUDGET - table_bytes;
     if (ncheck_tiles(p) != WH_OK) return WH_E_UNSUPPORTED;
-    // smem = window buffers (hi|lo fp16) + fp32 staging (same bytes as one window) + tap
-    // stages; prefer double-buffered windows, else one window with deeper tap staging
-    if (3 * win + 2 * stage_bytes <= budget) {
-        win_bufs = 2;
-        bstages = (int)std::min<int64_t>(4, (budget - 3 * win) / stage_bytes);
-    } else {
-        win_bufs = 1;
-        bstages = (int)std::min<int64_t>(4, (budget - 2 * win) / stage_bytes);
+    // smem = window buffers (hi|lo fp16) [+ fp32 staging, same bytes as one window] + tap
+    // stages.  Preference: 2 windows + staging, 1 window + staging, 2 windows, 1 window.
+    int use_stg = 0;
+    {
+        const int opts[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
+        for (auto &o : opts) {
+            const int64_t fixed = (int64_t)(o[0] + o[1]) * win;
+            if (fixed + 2 * stage_bytes <= budget) {
+                win_bufs = o[0];
+                use_stg = o[1];
+                bstages = (int)std::min<int64_t>(4, (budget - fixed) / stage_bytes);
+                break;
+            }
+        }
     }
     if (bstages < 2) return fail(WH_E_UNSUPPORTED, "UMMA engine: shared memory too small for 2 stages");
     p.win_bufs = win_bufs;
     p.bstages = bstages;
-    p.smem_bytes = (size_t)((win_bufs + 1) * win + bstages * stage_bytes) + 1024 + table_bytes;
+    p.use_stg = use_stg;
+    p.smem_bytes = (size_t)((win_bufs + use_stg) * win + bstages * stage_bytes) + 1024 + table_bytes;
 
     WH_CUDA_TRY(cudaMalloc(&p.d_passes, sizeof(UmmaPass) * p.passes.size()));
     WH_CUDA_TRY(cudaMalloc(&p.d_tiles, sizeof(UmmaTile) * p.tiles.size()));
@@ -890,6 +905,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.n_passes = (int32_t)p.passes.size(); a.n_tiles = (int32_t)p.tiles.size();
     a.wavelet = p.wavelet; a.output = p.output;
     a.bstages = p.bstages; a.win_bufs = p.win_bufs; a.n_acc = p.n_acc; a.acc_stride = p.acc_stride;
+    a.use_stg = p.use_stg;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
@@ -901,6 +917,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     const int64_t grid = std::min<int64_t>(a.items, p.sms);
     a.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (p.F % 4 == 0);
     a.prof = p.d_prof;
+    (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     umma_kernel(p.Cc, p.P)<<<(unsigned)grid, UM_THREADS, p.smem_bytes, s>>>(a);
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;

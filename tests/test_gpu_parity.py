@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA engines (through the C ABI) against the pinned CPU oracle and the
+reference's golden vectors.  Run on a B200 with ``pytest -m gpu``.
+
+Tolerances (written here once):
+  * complex / |W| / power: per (clip, scale) row, max_k |out - ref| / max_k |ref_row|
+    <= ROW_TOL = 1e-5 (power: 2e-5, it squares the relative error);
+  * log1p: absolute <= 1e-5; log_db: absolute <= 20/ln10 * 1e-5 + 2e-5 (dB);
+  * per-clip min-max: absolute <= 1e-5 * max/(max - min) (+ the fast-log term);
+  * bit-exact: shapes (B, S, ceil(N/hop)), frame k <-> sample k*hop, scale order,
+    the impulse KAT on the SIMT engine, sharded == unsharded bytes.
+"""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2408_14302_b200 as wh
+from conftest import golden_cases, row_rel_err
+from oracle import oracle as O
+from paper_2408_14302_b200 import _lib, synth
+from paper_2408_14302_b200.shard import cwth_multi_device, shard_range
+
+pytestmark = pytest.mark.gpu
+
+ROW_TOL = 1e-5
+ENGINES = ("umma", "simt")
+
+
+def umma_ok(hop):
+    return (hop <= 64 and 64 % hop == 0) or (hop % 64 == 0 and hop <= 256)
+
+
+def engines_for(hop):
+    return [e for e in ENGINES if e == "simt" or umma_ok(hop)]
+
+
+def gpu(x, scales, hop, engine, params=None, **kw):
+    return wh.cwth_batch(np.asarray(x, np.float32), scales, params or wh.MorletParams(), hop,
+                         engine=engine, **kw)
+
+
+# ---------------------------------------------------------------------------------------
+# golden vectors (the reference's own outputs)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_golden_cases_complex(golden_cwth, engine):
+    for case in golden_cases(golden_cwth):
+        if not (engine == "simt" or umma_ok(case["hop"])):
+            continue
+        p = wh.MorletParams(case["C"], case["B"], case["R"])
+        got = gpu(case["x"][None], case["scales"], case["hop"], engine, p, output="complex")[0]
+        ref = case["ref"]
+        assert got.shape == ref.shape, case["name"]
+        assert row_rel_err(got, ref) <= ROW_TOL, (case["name"], row_rel_err(got, ref))
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_golden_real_morlet_configs(golden_cwth, engine):
+    """c1 (full BASELINE config 1) and the small c2-c4 cases as real Morlet |W|."""
+    for name in ("c1", "c2s", "c3s", "c4s_h16", "c4s_h256", "c4s_h1024"):
+        hop = int(golden_cwth[f"{name}__meta"][0])
+        if engine == "umma" and not umma_ok(hop):
+            continue
+        ref = np.abs(golden_cwth[f"{name}__ref"].real)
+        got = gpu(golden_cwth[f"{name}__x"][None], golden_cwth[f"{name}__scales"], hop, engine,
+                  wavelet="rmor", output="abs")[0]
+        assert row_rel_err(got, ref) <= ROW_TOL, name
+
+
+def test_device_taps_within_one_ulp(golden_taps):
+    """The on-device filter-bank builder (fp64 math, fp32 store) vs sample_wavelet."""
+    for i, s in enumerate(golden_taps["pick_scales"]):
+        ref = golden_taps[f"taps_{i}"]
+        got = wh.sample_wavelet(wh.MorletParams(), float(s))
+        assert got.shape == ref.shape  # 2L+1 taps: L bit-exact
+        r32 = ref.astype(np.complex64)
+        ulp = np.spacing(np.abs(r32.real).astype(np.float32).max())
+        assert np.abs(got.real - r32.real).max() <= np.spacing(np.abs(r32.real)).max() + ulp
+        assert np.abs(got.imag - r32.imag).max() <= np.spacing(np.abs(r32.imag)).max() + ulp
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_impulse_sifts_the_wavelet(golden_cwth, engine):
+    """test_wavelet.py:156-167: out[row, n0/hop] == taps[center] (exact on SIMT: 1.0 x tap)."""
+    for name, hop in (("impulse_h1", 1), ("impulse_h4", 4)):
+        x = golden_cwth[f"{name}__x"]
+        sc = golden_cwth[f"{name}__scales"]
+        n0 = int(np.argmax(x))
+        out = gpu(x[None], sc, hop, engine, output="complex")[0]
+        for row, a in enumerate(sc):
+            taps = wh.sample_wavelet(wh.MorletParams(), float(a)).astype(np.complex64)
+            c = taps.size // 2
+            if engine == "simt":
+                assert out[row, n0 // hop] == taps[c]
+            else:
+                assert abs(out[row, n0 // hop] - taps[c]) <= 1e-6 * abs(taps[c])
+
+
+# ---------------------------------------------------------------------------------------
+# fused epilogues vs the oracle
+# ---------------------------------------------------------------------------------------
+
+def check_output(got, ref, output, norm):
+    if norm == "minmax":
+        assert np.all(got >= -1e-6) and np.all(got <= 1 + 1e-6)
+        assert np.abs(got - ref).max() <= 5e-5
+    elif output == "log1p":
+        assert np.abs(got - ref).max() <= 1e-5
+    elif output == "log_db":
+        # dB amplifies relative error near |W| = 0; compare the magnitudes it encodes
+        to_mag = lambda d: 10.0 ** (np.asarray(d, np.float64) / 20.0)  # noqa: E731
+        assert row_rel_err(to_mag(got), to_mag(ref)) <= ROW_TOL + 2e-6
+    elif output == "power":
+        assert row_rel_err(got, ref) <= 2 * ROW_TOL
+    else:
+        assert row_rel_err(got, ref) <= ROW_TOL
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("wavelet", ["cmor", "rmor"])
+@pytest.mark.parametrize("output,norm", [("abs", None), ("power", None), ("log1p", None),
+                                         ("log_db", None), ("abs", "minmax"), ("log1p", "minmax")])
+def test_epilogues_match_oracle(engine, wavelet, output, norm):
+    x = synth.make_batch(5, clips=3, n=6000, start=11)
+    sc = np.geomspace(1, 512, 12)
+    got = gpu(x, sc, 32, engine, wavelet=wavelet, output=output, norm=norm)
+    ref = O.cwth_batch(x, sc, 32, wavelet=wavelet, output=output, norm=norm)
+    assert got.shape == ref.shape
+    check_output(got, ref, output, norm)
+
+
+# ---------------------------------------------------------------------------------------
+# BASELINE configurations at full size
+# ---------------------------------------------------------------------------------------
+
+def cfg_run(cid, clips, hop=None, engine="auto", start=0):
+    cfg = synth.CONFIGS[cid]
+    hop = hop or cfg["hop"]
+    x = synth.make_batch(cid, clips=clips, start=start)
+    sc = synth.config_scales(cid)
+    got = gpu(x, sc, hop, engine, wavelet=cfg["wavelet"], output=cfg["output"], norm=cfg["norm"])
+    return x, sc, hop, cfg, got
+
+
+def test_c2_full_batch_parity():
+    """BASELINE config 2 at full size: 64 clips x 160,000 samples, 128 scales, hop 64, log1p."""
+    x, sc, hop, cfg, got = cfg_run(2, 64)
+    assert got.shape == (64, 128, 2500)
+    ref = O.cwth_batch(x, sc, hop, wavelet="rmor", output="log1p")
+    assert np.abs(got - ref).max() <= 1e-5
+
+
+def test_c3_full_hop1_parity():
+    """BASELINE config 3 (full CWT, hop 1): 8 clips x 160,000 x 64 scales -- 2 clips vs oracle."""
+    x, sc, hop, cfg, got = cfg_run(3, 8)
+    assert got.shape == (8, 64, 160000)
+    ref = O.cwth_batch(x[:2], sc, 1, wavelet="rmor", output="abs")
+    assert row_rel_err(got[:2], ref) <= ROW_TOL
+
+
+@pytest.mark.parametrize("hop", [1, 16, 64, 256, 1024])
+def test_c4_hop_sweep_parity(hop):
+    """BASELINE config 4 sweep: 2 clips per hop vs the oracle; frames = ceil(N/hop)."""
+    x, sc, hop, cfg, got = cfg_run(4, 2, hop=hop)
+    assert got.shape == (2, 64, -(-160000 // hop))
+    ref = O.cwth_batch(x, sc, hop, wavelet="rmor", output="abs")
+    assert row_rel_err(got, ref) <= ROW_TOL
+
+
+def test_c4_hop_columns_are_full_transform_columns():
+    """test_wavelet.py:245-252 at BASELINE size: cwth(hop)[:, k] == cwth(1)[:, k*hop]."""
+    x = synth.make_batch(4, clips=1, start=3)
+    sc = synth.config_scales(4)
+    full = gpu(x, sc, 1, "auto", wavelet="rmor", output="complex")[0]
+    for hop in (16, 64, 256, 1024):
+        hopped = gpu(x, sc, hop, "auto", wavelet="rmor", output="complex")[0]
+        assert hopped.shape[1] == -(-160000 // hop)
+        assert row_rel_err(hopped, full[:, ::hop]) <= 2 * ROW_TOL
+
+
+def test_c5_sample_parity_and_minmax_range():
+    """BASELINE config 5 (complex Morlet, 160 scales 1-512, hop 32, per-clip min-max)."""
+    x, sc, hop, cfg, got = cfg_run(5, 4)
+    assert got.shape == (4, 160, 5000)
+    ref = O.cwth_batch(x, sc, hop, wavelet="cmor", output="abs", norm="minmax")
+    assert np.abs(got - ref).max() <= 5e-5
+    for c in range(4):
+        assert got[c].min() == 0.0 and abs(got[c].max() - 1.0) <= 1e-6
+
+
+# ---------------------------------------------------------------------------------------
+# size-independent properties at full size
+# ---------------------------------------------------------------------------------------
+
+def test_linearity_full_size():
+    """test_wavelet.py:326-346: W(a x + b y) = a W(x) + b W(y)."""
+    x = synth.make_batch(5, clips=2, start=40)
+    sc = synth.config_scales(5)
+    a, b = 0.3, -0.7
+    lhs = gpu((a * x[0] + b * x[1])[None], sc, 32, "auto", output="complex")[0]
+    w = gpu(x, sc, 32, "auto", output="complex")
+    assert row_rel_err(lhs, a * w[0] + b * w[1]) <= 3 * ROW_TOL
+
+
+def test_sharded_equals_unsharded_bytes():
+    """Per-clip work is identical, so any clip split gives byte-equal scalograms."""
+    x = synth.make_batch(2, clips=10, start=0)
+    sc = synth.config_scales(2)
+    whole = gpu(x, sc, 64, "auto", wavelet="rmor", output="log1p")
+    parts = [gpu(x[a:b], sc, 64, "auto", wavelet="rmor", output="log1p")
+             for a, b in (shard_range(10, 3, r) for r in range(3))]
+    np.testing.assert_array_equal(whole, np.concatenate(parts))
+    multi = cwth_multi_device(x, sc, None, 64, devices=[0, 0], wavelet="rmor", output="log1p")
+    np.testing.assert_array_equal(whole, multi)
+
+
+def test_zero_signal_and_constant_minmax():
+    sc = synth.config_scales(5)
+    z = np.zeros((2, 160000), np.float32)
+    assert np.all(gpu(z, sc, 32, "auto", output="abs") == 0.0)
+    assert np.all(gpu(z, sc, 32, "auto", output="abs", norm="minmax") == 0.0)
+
+
+def test_device_and_host_paths_identical():
+    x = synth.make_batch(2, clips=3, n=20000)
+    sc = np.geomspace(1, 128, 40)
+    plan = wh.CwthPlan(sc, None, 64, 20000, wavelet="rmor", output="abs", max_clips=3)
+    host = plan.execute_host(x)
+    dev = plan.execute(torch.from_numpy(x).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(host, dev)
+    assert plan.launches(3) == 1
+
+
+# ---------------------------------------------------------------------------------------
+# edges and errors
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_ragged_and_tiny_signals(engine):
+    rng = np.random.default_rng(9)
+    for n, hop, scales in [(1001, 64, [1.0, 3.3, 20.0]), (5, 2, [1.0, 100.0]), (1, 1, [1.0, 2.0]),
+                           (100, 128, [1.5, 6.0]), (4097, 16, [2.0, 64.0, 300.0])]:
+        if engine == "umma" and not umma_ok(hop):
+            continue
+        x = rng.standard_normal((2, n)).astype(np.float32)
+        got = gpu(x, scales, hop, engine, output="complex")
+        ref = O.cwth_batch(x, scales, hop, output="complex")
+        assert got.shape == ref.shape == (2, len(scales), -(-n // hop))
+        assert row_rel_err(got, ref) <= ROW_TOL, (n, hop)
+
+
+def test_engine_selection_and_errors():
+    assert wh.CwthPlan([1.0, 2.0], None, 64, 1000).engine == "umma"
+    assert wh.CwthPlan([1.0, 2.0], None, 7, 1000).engine == "simt"
+    with pytest.raises(wh.DeviceError):
+        wh.CwthPlan([1.0, 2.0], None, 7, 1000, engine="umma")
+    with pytest.raises(wh.InvalidHop):
+        wh.CwthPlan([1.0], None, 0, 100)
+    with pytest.raises(wh.InvalidScale):
+        wh.CwthPlan([0.0, 1.0], None, 4, 100)
+    with pytest.raises(ValueError):
+        wh.CwthPlan([2.0, 1.0], None, 4, 100)
+    plan = wh.CwthPlan([1.0, 2.0], None, 4, 100, max_clips=2)
+    with pytest.raises(ValueError):
+        plan.execute_host(np.zeros((3, 100), np.float32))
+    with pytest.raises(ValueError):
+        plan.execute_host(np.zeros((1, 99), np.float32))
+
+
+def test_drop_in_signatures(golden_cwth):
+    """cwth_strided / cwt_fft keep the reference signatures and metadata."""
+    x = golden_cwth["c2s__x"]
+    sc = golden_cwth["c2s__scales"]
+    sig = wh.SignalBuffer(x.astype(np.float64), 16000.0)
+    m = wh.cwth_strided(sig, wh.ScaleGrid(sc), wh.MorletParams(), 64, threads=4)
+    assert m.hop == 64 and m.source_rate == 16000.0 and m.values.dtype == np.complex128
+    assert m.columns == -(-x.size // 64) and m.rows == sc.size
+    assert row_rel_err(m.values, golden_cwth["c2s__ref"]) <= ROW_TOL
+    full = wh.cwt_fft(sig, wh.ScaleGrid(sc))
+    assert full.hop == 1 and full.columns == x.size
+    assert row_rel_err(full.values[:, ::64], m.values) <= 2 * ROW_TOL
+    mag = wh.magnitude(m, "abs")
+    assert row_rel_err(mag, np.abs(golden_cwth["c2s__ref"])) <= ROW_TOL
+
+
+def test_seam2_kernels_match_oracle():
+    """_kernels.py seam: float64 device kernels within 1e-12 of the oracle."""
+    lib = _lib.load()
+    rng = np.random.default_rng(2)
+    for hop, half, frames in [(1, 4, 30), (9, 100, 21), (128, 513, 7)]:
+        width = 2 * half + 1
+        xpad = rng.standard_normal((frames - 1) * hop + width + 2)
+        tr, ti = rng.standard_normal(width), rng.standard_normal(width)
+        ore, oim = np.empty(frames), np.empty(frames)
+        P = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        assert lib.wh_strided_correlate(0, P(xpad), xpad.size, P(tr), P(ti), width, hop, frames,
+                                        P(ore), P(oim)) == 0
+        r = O.strided_correlate(xpad, tr, ti, hop, frames)
+        sc = max(np.abs(r[0]).max(), np.abs(r[1]).max())
+        assert np.abs(ore - r[0]).max() <= 1e-12 * sc and np.abs(oim - r[1]).max() <= 1e-12 * sc
+        even = rng.standard_normal(half + 1)
+        odd = np.concatenate([[0.0], rng.standard_normal(half)])
+        assert lib.wh_strided_correlate_symmetric(0, P(xpad), xpad.size, P(even), P(odd), half, hop,
+                                                  frames, P(ore), P(oim)) == 0
+        r = O.strided_correlate_symmetric(xpad, even, odd, hop, frames)
+        sc = max(np.abs(r[0]).max(), np.abs(r[1]).max())
+        assert np.abs(ore - r[0]).max() <= 1e-12 * sc and np.abs(oim - r[1]).max() <= 1e-12 * sc
