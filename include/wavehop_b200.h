@@ -106,9 +106,13 @@ int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im,
                  int64_t *half);
 
 /* Diagnostics: enable (1) / disable (0) per-role wait-cycle counters of the UMMA engine
- * kernel and read-and-reset them (16 counters: role*4 + {wait0, wait1, wait2, total}, roles
- * producer, MMA, converter, epilogue; summed over CTAs and warps).  counters may be NULL. */
+ * kernel and read-and-reset them (20 counters: role*4 + {wait0, wait1, wait2, total}, roles
+ * producer, MMA, converter, epilogue, relay; summed over CTAs and warps).  counters may be NULL. */
 int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n);
+
+/* Diagnostics: CTA-0 timeline of the UMMA engine kernel (clock64 stamps, [16 events][32
+ * units]); enable / disable and read (events may be NULL). */
+int wh_plan_trace(wh_plan *plan, int32_t enable, int64_t *events, int32_t n);
 
 /* The hot path.  x_dev: device float32 [clips][ld_x] (ld_x >= n_samples);
  * out_dev: device [clips][n_scales][frames] float32 (real outputs) or

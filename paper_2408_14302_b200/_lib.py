@@ -50,6 +50,7 @@ SIGNATURES = {
     "wh_plan_launches": (ctypes.c_int, [_p, _i64, _pi64]),
     "wh_plan_taps": (ctypes.c_int, [_p, _i32, _p, _p, _i64, _pi64]),
     "wh_plan_profile": (ctypes.c_int, [_p, _i32, _p, _i32]),
+    "wh_plan_trace": (ctypes.c_int, [_p, _i32, _p, _i32]),
     "wh_execute": (ctypes.c_int, [_p, _p, _i64, _i64, _p, _p]),
     "wh_execute_host": (ctypes.c_int, [_p, _p, _i64, _p]),
     "wh_strided_correlate": (ctypes.c_int, [ctypes.c_int, _p, _i64, _p, _p, _i64, _i64, _i64, _p, _p]),

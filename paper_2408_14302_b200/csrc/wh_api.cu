@@ -195,8 +195,8 @@ static void plan_free(Plan *p) {
     cudaSetDevice(p->device);
     cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
     cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
-    cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_bank); cudaFree(p->d_scale_pow);
-    cudaFree(p->d_minmax); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof);
+    cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow);
+    cudaFree(p->d_minmax); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     cudaSetDevice(cur);
     delete p;
@@ -419,19 +419,43 @@ int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n
     cudaGetDevice(&prev);
     WH_CUDA_TRY(cudaSetDevice(p->device));
     if (!p->d_prof) {
-        WH_CUDA_TRY(cudaMalloc(&p->d_prof, sizeof(unsigned long long) * 16));
-        WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 16));
+        WH_CUDA_TRY(cudaMalloc(&p->d_prof, sizeof(unsigned long long) * 20));
+        WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 20));
     }
     if (counters && n > 0) {
-        unsigned long long h[16];
+        unsigned long long h[20];
         WH_CUDA_TRY(cudaDeviceSynchronize());
         WH_CUDA_TRY(cudaMemcpy(h, p->d_prof, sizeof h, cudaMemcpyDeviceToHost));
-        for (int i = 0; i < n && i < 16; ++i) counters[i] = h[i];
-        WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 16));
+        for (int i = 0; i < n && i < 20; ++i) counters[i] = h[i];
+        WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 20));
     }
     if (!enable) {
-        cudaFree(p->d_prof);
+        cudaFree(p->d_prof); cudaFree(p->d_trace);
         p->d_prof = nullptr;
+    }
+    cudaSetDevice(prev);
+    return WH_OK;
+}
+
+int wh_plan_trace(wh_plan *plan, int32_t enable, int64_t *events, int32_t n) {
+    if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    WH_CUDA_TRY(cudaSetDevice(p->device));
+    if (!p->d_trace) {
+        WH_CUDA_TRY(cudaMalloc(&p->d_trace, sizeof(long long) * 16 * 32));
+        WH_CUDA_TRY(cudaMemset(p->d_trace, 0, sizeof(long long) * 16 * 32));
+    }
+    if (events && n > 0) {
+        long long h[16 * 32];
+        WH_CUDA_TRY(cudaDeviceSynchronize());
+        WH_CUDA_TRY(cudaMemcpy(h, p->d_trace, sizeof h, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n && i < 16 * 32; ++i) events[i] = h[i];
+    }
+    if (!enable) {
+        cudaFree(p->d_trace);
+        p->d_trace = nullptr;
     }
     cudaSetDevice(prev);
     return WH_OK;

@@ -40,15 +40,22 @@ struct SimtItem {       // one CTA of work: group g, frames [k0, k0 + tf)
 struct UmmaPass {
     int32_t tile_begin, tile_end;  // range in the tile table
     int32_t s0, ns;                // scales covered by the pass
-    int32_t cols;                  // TMEM columns (multiple of 16, <= 256)
-    int32_t pad_;
+    int32_t cols;                  // TMEM columns (multiple of 16, <= 128)
+    int32_t group_begin, group_end;  // range in the group table
 };
 struct UmmaTile {                  // one K-step (64 taps) of one pass
     int32_t k;                     // K-step index (g in [64k, 64k+64))
     int32_t c0;                    // first active column (multiple of 16)
     int32_t ncols;                 // cols - c0
-    int32_t pad_;
-    int64_t byte_off;              // offset of the hi|lo tile image in the bank
+    int32_t in_off;                // byte offset of the tile inside its group's CTA block
+    int64_t byte_off;              // bank offset of the tile (CTA-0 block of its group)
+    int64_t blk1_delta;            // cg = 2: bytes from the CTA-0 block to the CTA-1 block
+};
+struct UmmaGroup {                 // consecutive tiles of a pass fetched by one bulk copy
+    int32_t tile_begin, tile_end;
+    int32_t cta_bytes;             // bytes each CTA copies
+    int32_t pad_;                  // resident bank: the group's smem offset in the ring
+    int64_t bank_off;              // bank offset of the group's CTA-0 block
 };
 
 struct Plan {
@@ -85,18 +92,24 @@ struct Plan {
     int32_t rows_total = 0, row_tiles = 0;
     std::vector<UmmaPass> passes;
     std::vector<UmmaTile> tiles;
+    std::vector<UmmaGroup> groups_u;
     UmmaPass *d_passes = nullptr;
     UmmaTile *d_tiles = nullptr;
+    UmmaGroup *d_groups_u = nullptr;
     uint8_t *d_bank = nullptr;
     int64_t bank_bytes = 0;
     float *d_scale_pow = nullptr;  // per scale 2^-f_s
     std::vector<int32_t> fexp;
-    int32_t bstages = 2, win_bufs = 2;
+    int32_t bstages = 2, win_bufs = 2;     // bstages: full-width tiles the ring holds (info)
+    int64_t ring_bytes = 0;                // tap-tile ring capacity
     int32_t n_acc = 2, acc_stride = 256;   // TMEM accumulator buffers, columns per buffer
     int32_t use_stg = 1;                   // fp32 window staged by cp.async.bulk
+    int32_t cg = 2;                        // CTAs per MMA (tcgen05 cta_group)
+    int32_t resident = 0;                  // whole tap bank resident in smem
     size_t smem_bytes = 0;     // dynamic shared memory of the engine kernel
 
     unsigned long long *d_prof = nullptr;  // diagnostics counters (wh_plan_profile)
+    long long *d_trace = nullptr;          // diagnostics timeline (wh_plan_trace)
 
     // per-clip min/max (ordered-uint keys) for WH_NORM_MINMAX
     uint32_t *d_minmax = nullptr;  // [max_clips][2]

@@ -17,7 +17,7 @@
 //   in fp32 (the dropped xl*tl term is ~2^-22 relative), then D * 2^-(e+f).
 //
 // CTA roles (256 threads, 1 CTA per SM, persistent over (clip, row-tile) items):
-//   warp 0      producer: cp.async.bulk of tap tiles into a bstages-deep ring
+//   warp 0      producer: cp.async.bulk of tap tiles into a byte ring of variable-size slots
 //   warp 1      TMEM allocator + MMA issuer (one elected thread)
 //   warps 2-3   converters: window max -> exponent -> hi/lo fp16 swizzled window
 //   warps 4-7   epilogue: tcgen05.ld -> scale, |W| / log1p / ... -> global stores,
@@ -27,6 +27,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "wh_internal.h"
 
@@ -34,31 +36,39 @@ namespace wh {
 
 static constexpr int UM_CONV_WARPS = 4;
 static constexpr int UM_CONV_THREADS = 32 * UM_CONV_WARPS;
-static constexpr int UM_THREADS = 64 + UM_CONV_THREADS + 128;  // producer, MMA, converters, epilogue
-static constexpr int UM_MAX_STAGES = 6;
+static constexpr int UM_EPI_WARPS = 8;  // 2 per TMEM lane quadrant
+static constexpr int UM_THREADS = 64 + UM_CONV_THREADS + 32 * UM_EPI_WARPS;  // producer, MMA, converters, epilogue
+static constexpr int UM_SLOTS = 16;  // in-flight tap tiles (ring slots)
 static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
 
 struct UmmaArgs {
     const float *x;
     int64_t ld_x, N, F, hop;
     int64_t items;              // clips * row_tiles
+    int64_t clips;
     int32_t row_tiles, V, P, Cc, panels, Qlo, win_rows, S;
-    int32_t n_passes, n_tiles, wavelet, output, bstages, win_bufs, vec_ok;
+    int32_t n_passes, n_tiles, wavelet, output, win_bufs, vec_ok;
     int32_t n_acc, acc_stride;          // accumulator buffers; columns per buffer (main|corr)
     int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
+    int32_t resident;                   // the whole tap bank lives in the ring (loaded once)
+    int32_t cpr_shift;                  // log2(8-sample chunks per window row) = log2(panels * 8)
     const UmmaPass *passes;
     const UmmaTile *tiles;
+    const UmmaGroup *groups;
+    int32_t n_groups;
     const uint8_t *bank;
     const float *scale_pow;
     void *out;
     uint32_t *minmax;
-    uint32_t stage_bytes, win_half_bytes;
+    uint32_t ring_bytes, win_half_bytes;
     int32_t out_vec_ok;             // output base 16B aligned and F % 4 == 0
     unsigned long long *prof;       // optional per-role wait counters (wh_plan_profile)
+    int32_t dbg;                    // diagnostics: 1 no epilogue work, 2 no converter work, 4 no MMA
+    long long *trace;               // diagnostics: CTA-0 timeline [event][unit] (WH_UMMA_TRACE)
 };
 
 // Wait-cycle counters (diagnostics): index = role * 4 + slot; slot 3 = total cycles.
-enum { PR_PROD = 0, PR_MMA = 1, PR_CONV = 2, PR_EPI = 3 };
+enum { PR_PROD = 0, PR_MMA = 1, PR_CONV = 2, PR_EPI = 3, PR_RELAY = 4 };
 struct ProfAcc {
     unsigned long long c[4] = {0, 0, 0, 0};
     long long t0 = 0;
@@ -74,14 +84,26 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+#ifdef WH_WAIT_HINT
+    // suspend-time hint (ns): the waiting thread sleeps until the phase completes or the hint
     uint32_t done = 0;
     while (!done) {
         asm volatile(
             "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
-            : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
+            : "r"(smem_u32(b)), "r"(parity), "r"((uint32_t)WH_WAIT_HINT)
             : "memory");
     }
+#else
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    }
+#endif
 }
 __device__ __forceinline__ void mbar_wait_p(uint64_t *b, uint32_t parity, ProfAcc &pa, int slot,
                                             bool on) {
@@ -98,6 +120,12 @@ __device__ __forceinline__ void prof_flush(const ProfAcc &pa, unsigned long long
     for (int i = 0; i < 3; ++i) atomicAdd(prof + role * 4 + i, pa.c[i]);
     atomicAdd(prof + role * 4 + 3, (unsigned long long)(clock64() - pa.t0));
 }
+// diagnostics timeline (CTA 0 only): event e of unit u
+#define WH_TRACE(e, u)                                                                      \
+    do {                                                                                    \
+        if (A.trace && blockIdx.x == 0 && (u) < 32 && lane == 0) A.trace[(e) * 32 + (u)] = clock64(); \
+    } while (0)
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -113,10 +141,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t *b) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
-                 : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -124,16 +148,6 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
     return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
            ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ uint32_t idesc_f16(uint32_t n) {
-    // D f32 (bit 4), A/B f16 (0), K-major A/B, N>>3 at [17,23), M>>4 at [24,29), M = 128
-    return (1u << 4) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
@@ -145,6 +159,68 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+template <int CG>
+__device__ __forceinline__ void cta_pair_sync() {
+    if constexpr (CG == 2) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        __syncthreads();
+    }
+}
+// relaxed remote arrive (tap-tile relay: the data was written by the async proxy and its
+// local completion was observed by the relay's wait)
+__device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t *b) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(b)));
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// arrive on the barrier at the same smem offset in the leader CTA (rank 0) of the pair
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *b) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(b)));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(0u)
+        : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+    // accumulate always: the epilogue re-zeroes every accumulator buffer it drains
+    if constexpr (CG == 2)
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem), "l"(a), "l"(b),
+                     "r"(idesc), "r"(1u));
+    else
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem), "l"(a), "l"(b),
+                     "r"(idesc), "r"(1u));
+}
+template <int CG>
+__device__ __forceinline__ uint32_t idesc_f16(uint32_t n) {
+    // D f32 (bit 4), A/B f16 (0), K-major A/B, N>>3 at [17,23), M>>4 at [24,29), M = 128*CG
+    return (1u << 4) | ((n >> 3) << 17) | (((128u * CG) >> 4) << 24);
+}
+template <int CG>
+__device__ __forceinline__ void umma_commit(uint64_t *b) {
+    if constexpr (CG == 2)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(b)),
+            "h"((uint16_t)3)
+            : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+                     : "memory");
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -239,50 +315,62 @@ __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nval
     }
 }
 
-// One accumulator buffer (a pass of ns scales) -> global, for this thread's row.
+// One accumulator buffer (a pass of ns scales) -> global, for this thread's row.  The two
+// epilogue warps of a TMEM lane quadrant split the 16-column units (half = 0 / 1); each
+// re-zeroes the main and correction columns it has read.
 template <int CC, int P, int OUT>
-__device__ __forceinline__ void epi_pass(const UmmaArgs &A, uint32_t tbase, uint32_t cbase, int s0, int ns,
-                                         int cols, int64_t b, int64_t frame0, int nvalid, float e, bool vec,
-                                         float &lmin, float &lmax) {
+__device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, uint32_t tbase, uint32_t cbase,
+                                         int s0, int ns, int cols, int half, int64_t b, int64_t frame0,
+                                         int nvalid, float e, bool vec, float &lmin, float &lmax) {
     constexpr int CP = CC * P;
-    // NOTE: tcgen05.ld is warp-collective (.sync.aligned): every load below is executed by
-    // all 32 lanes; only the stores depend on the lane's row (nvalid).
+    // NOTE: tcgen05.ld/st are warp-collective (.sync.aligned): every TMEM access below is
+    // executed by all 32 lanes; only the global stores depend on the lane's row (nvalid).
     const int64_t F = A.F;
-    int64_t o = (b * A.S + s0) * F + frame0;  // element index of (scale s0, frame0)
+    const int64_t o0 = (b * A.S + s0) * F + frame0;  // element index of (scale s0, frame0)
     if constexpr (CP <= 16) {
         constexpr int SPU = 16 / CP;  // whole scales per 16-column unit
-        for (int u0 = 0, sl0 = 0; u0 < cols; u0 += 16, sl0 += SPU) {
-            float v[16], wr[16], w[16];
+        for (int u0 = 16 * half; u0 < cols; u0 += 32) {
+            const int sl0 = u0 / CP;
+            float v[16], wr[16];
             tmem_ld16x2(tbase + u0, cbase - u0, v, wr);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) w[i] = wr[15 - i];
+            tmem_st16_zero(tbase + u0);
+            tmem_st16_zero(cbase - u0);
+            if (nvalid <= 0) continue;
+            float re[SPU][P], im[SPU][P];
 #pragma unroll
             for (int q = 0; q < SPU; ++q) {
-                const int sl = sl0 + q;
-                if (sl < ns && nvalid > 0) {
-                    const float f = e * __ldg(A.scale_pow + s0 + sl);
-                    float re[P], im[P];
+                const float f = (sl0 + q < ns) ? e * spow[s0 + sl0 + q] : 0.0f;
 #pragma unroll
-                    for (int r = 0; r < P; ++r) {
-                        re[r] = (v[q * CP + r] + w[q * CP + r]) * f;
-                        im[r] = (CC == 2) ? (v[q * CP + (P + r) % CP] + w[q * CP + (P + r) % CP]) * f : 0.0f;
-                    }
-                    store_run<P, CC, OUT>(A, o + (int64_t)sl * F, nvalid, re, im, vec, lmin, lmax);
+                for (int r = 0; r < P; ++r) {
+                    re[q][r] = (v[q * CP + r] + wr[15 - (q * CP + r)]) * f;
+                    if constexpr (CC == 2)
+                        im[q][r] = (v[q * CP + P + r] + wr[15 - (q * CP + P + r)]) * f;
+                    else
+                        im[q][r] = 0.0f;
                 }
             }
+            const bool full = (sl0 + SPU <= ns);
+#pragma unroll
+            for (int q = 0; q < SPU; ++q)
+                if (full || sl0 + q < ns)
+                    store_run<P, CC, OUT>(A, o0 + (int64_t)(sl0 + q) * F, nvalid, re[q], im[q], vec, lmin, lmax);
         }
     } else {
-        // P >= 16: per scale, 16-phase chunks of re (and im)
-        for (int sl = 0; sl < ns; ++sl) {
-            const float f = e * __ldg(A.scale_pow + s0 + sl);
+        // P >= 16: per scale, 16-phase chunks of re (and im); the two warps take alternate scales
+        for (int sl = half; sl < ns; sl += 2) {
+            const float f = e * spow[s0 + sl];
 #pragma unroll 1
             for (int r0 = 0; r0 < P; r0 += 16) {
                 float re[16], im[16], w[16];
                 tmem_ld16x2(tbase + sl * CP + r0, cbase - (sl * CP + r0), re, w);
+                tmem_st16_zero(tbase + sl * CP + r0);
+                tmem_st16_zero(cbase - (sl * CP + r0));
 #pragma unroll
                 for (int i = 0; i < 16; ++i) re[i] = (re[i] + w[15 - i]) * f;
                 if constexpr (CC == 2) {
                     tmem_ld16x2(tbase + sl * CP + P + r0, cbase - (sl * CP + P + r0), im, w);
+                    tmem_st16_zero(tbase + sl * CP + P + r0);
+                    tmem_st16_zero(cbase - (sl * CP + P + r0));
 #pragma unroll
                     for (int i = 0; i < 16; ++i) im[i] = (im[i] + w[15 - i]) * f;
                 } else {
@@ -290,100 +378,190 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, uint32_t tbase, uint
                     for (int i = 0; i < 16; ++i) im[i] = 0.0f;
                 }
                 const int nv = nvalid - r0 < 16 ? nvalid - r0 : 16;
-                if (nv > 0) store_run<16, CC, OUT>(A, o + (int64_t)sl * F + r0, nv, re, im, vec, lmin, lmax);
+                if (nv > 0) store_run<16, CC, OUT>(A, o0 + (int64_t)sl * F + r0, nv, re, im, vec, lmin, lmax);
             }
         }
+        // a pass whose scale count is odd leaves padding columns to the other warp: zero
+        // the columns [ns*CP, cols) (if any) from warp half 0
+        if (half == 0)
+            for (int c = ns * CP; c < cols; c += 16) {
+                tmem_st16_zero(tbase + c);
+                tmem_st16_zero(cbase - c);
+            }
     }
 }
 
 // ---- the kernel --------------------------------------------------------------------------
-template <int CC, int P>
+template <int CC, int P, int CG>
 __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ UmmaArgs A) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ __align__(8) uint64_t b_full[UM_MAX_STAGES], b_empty[UM_MAX_STAGES];
+    __shared__ __align__(8) uint64_t b_full[UM_SLOTS], b_empty[UM_SLOTS];
+    __shared__ uint64_t s_vstart[UM_SLOTS];  // producer-private: ring start of in-flight slots
     __shared__ __align__(8) uint64_t win_full[2], win_empty[2], acc_full[2], acc_empty[2];
-    __shared__ float wexp[2], accexp[2];
+    __shared__ float xring[4];  // per-unit window exponent 2^-e, written by the converters
     __shared__ float red[UM_CONV_WARPS];
     __shared__ __align__(8) uint64_t stg_full;
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // 0 = leader (issues the MMAs)
+    const bool leader = rank == 0;
+    // work units: (clip, CG consecutive 128-row tiles); CTA `rank` of a pair takes tile
+    // CG*j + rank.  All roles walk the same unit sequence.
+    const int64_t u0 = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t ustride = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+    const int64_t tpu = (A.row_tiles + CG - 1) / CG;
+    const int64_t n_units = A.clips * tpu;
+    auto unit_tile = [&](int64_t u, int64_t &b, int64_t &tile) {
+        b = u / tpu;
+        tile = CG * (u % tpu) + rank;
+    };
     const uint32_t WH = A.win_half_bytes;               // bytes of one (hi or lo) window
     uint8_t *win_base = smem;                            // [win_bufs][hi|lo][panels][rows][128]
     uint8_t *stage_base = smem + (size_t)A.win_bufs * 2 * WH;
     const uint32_t panel_bytes = (uint32_t)A.win_rows * 128u;
-    // pass / tile tables (compact) after the fp32 staging buffer
-    int4 *s_pass = reinterpret_cast<int4 *>(stage_base + (size_t)A.bstages * A.stage_bytes +
+    // pass / tile tables (compact) after the tap stages (and the fp32 staging buffer)
+    int4 *s_pass = reinterpret_cast<int4 *>(stage_base + (size_t)A.ring_bytes +
                                             (A.use_stg ? 2 * (size_t)WH : 0));
-    uint2 *s_tile = reinterpret_cast<uint2 *>(s_pass + A.n_passes);
+    int4 *s_group = s_pass + A.n_passes;
+    uint2 *s_tile = reinterpret_cast<uint2 *>(s_group + A.n_groups);
+    int *s_goff = reinterpret_cast<int *>(s_tile + A.n_tiles);  // resident: smem offset per group
+    float *s_spow = reinterpret_cast<float *>(s_goff + A.n_groups);
+    for (int i = threadIdx.x; i < A.S; i += blockDim.x) s_spow[i] = A.scale_pow[i];
     for (int i = threadIdx.x; i < A.n_passes; i += blockDim.x) {
         const UmmaPass ps = A.passes[i];
-        s_pass[i] = make_int4(ps.tile_begin, ps.tile_end, ps.s0 | (ps.ns << 16), ps.cols);
+        s_pass[i] = make_int4(ps.group_begin, ps.group_end, ps.s0 | (ps.ns << 16), ps.cols);
+    }
+    for (int i = threadIdx.x; i < A.n_groups; i += blockDim.x) {
+        const UmmaGroup g = A.groups[i];
+        s_group[i] = make_int4(g.tile_begin, g.tile_end, (int)(uint32_t)(g.bank_off >> 7), g.cta_bytes);
+        s_goff[i] = g.pad_;
     }
     for (int i = threadIdx.x; i < A.n_tiles; i += blockDim.x) {
         const UmmaTile tl = A.tiles[i];
-        s_tile[i] = make_uint2((uint32_t)tl.k | ((uint32_t)tl.c0 << 16) | ((uint32_t)tl.ncols << 24),
-                               (uint32_t)(tl.byte_off >> 8));
+        // window row shift q and panel of this K-step's A operand (k*64 = q*V + panel*64)
+        const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)A.V, panel = (kg % (uint32_t)A.V) >> 6;
+        s_tile[i] = make_uint2(q | (panel << 12) | ((uint32_t)tl.c0 << 16) | ((uint32_t)tl.ncols << 24),
+                               (uint32_t)tl.in_off);
     }
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < A.bstages; ++i) {
-            mbar_init(&b_full[i], 1);
+        for (int i = 0; i < UM_SLOTS; ++i) {
+            mbar_init(&b_full[i], (CG == 2 && leader) ? 2 : 1);  // + the peer's relay
             mbar_init(&b_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&win_full[i], UM_CONV_WARPS);
+            mbar_init(&win_full[i], UM_CONV_WARPS + ((CG == 2 && leader) ? 1 : 0));
             mbar_init(&win_empty[i], 1);
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 4);
+            mbar_init(&acc_empty[i], UM_EPI_WARPS * CG);  // epilogue warps of both CTAs (leader's copy)
         }
         mbar_init(&stg_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&tmem_base_sh)), "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&tmem_base_sh)), "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    if (warp >= 2 + UM_CONV_WARPS) {
+        // epilogue warps zero both accumulator buffers of their lane quadrant: every MMA
+        // accumulates (accumulate = 1), columns a pass never touches stay 0
+        const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t ehalf = (uint32_t)((warp - 2 - UM_CONV_WARPS) >> 2);
+        for (uint32_t c = 256 * ehalf; c < 256 * ehalf + 256; c += 16) tmem_st16_zero(tq + c);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cta_pair_sync<CG>();
+    tc_fence_after();
     const bool pon = A.prof != nullptr;
     ProfAcc pa;
     pa.start();
 
     if (warp == 0) {
-        // ===================== producer: tap tiles (whole warp, one elected lane) ====
-        uint32_t st = 0, ph = 0;
-        for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
+        // ===================== producer: this CTA's half of each tap tile =============
+        // Tiles have different sizes (nc columns), so the stage buffer is a byte ring of
+        // UM_SLOTS variable-size slots: virtual offsets grow monotonically, a tile never
+        // straddles the physical end, and a slot is reused once the MMAs that read the
+        // oldest bytes in the way have committed.
+        if (A.resident) {
+            // one barrier for the whole bank: arm it with all bytes, then copy every group
+            if (elect_one()) {
+                uint32_t total = 0;
+                for (int gi = 0; gi < A.n_groups; ++gi) total += (uint32_t)s_group[gi].w;
+                mbar_expect_tx(&b_full[0], total);
+                for (int gi = 0; gi < A.n_groups; ++gi) {
+                    const int4 gr = s_group[gi];
+                    bulk_g2s(stage_base + s_goff[gi], A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * gr.w,
+                             (uint32_t)gr.w, &b_full[0]);
+                }
+            }
+            __syncwarp();
+        }
+        uint64_t vhead = 0;   // virtual (monotonic) ring offset
+        uint32_t phys = 0;    // vhead % RING, tracked incrementally
+        uint32_t seq = 0, tail = 0;
+        const uint32_t RING = A.ring_bytes;
+        for (int64_t item = A.resident ? n_units : u0; item < n_units; item += ustride) {
             for (int p = 0; p < A.n_passes; ++p) {
                 const int4 pinfo = s_pass[p];
-                for (int t = pinfo.x; t < pinfo.y; ++t) {
-                    const uint2 tt = s_tile[t];
-                    const uint32_t ncols = tt.x >> 24;
-                    mbar_wait_p(&b_empty[st], ph ^ 1, pa, 0, pon);
+                for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
+                    const int4 gr = s_group[gi];
+                    const uint32_t bytes = (uint32_t)gr.w;
+                    uint64_t v = vhead;
+                    if (phys + bytes > RING) {  // never straddle the physical end
+                        v += RING - phys;
+                        phys = 0;
+                    }
+                    const uint64_t vend = v + bytes;
+                    while (tail < seq && (seq - tail >= (uint32_t)UM_SLOTS || s_vstart[tail % UM_SLOTS] + RING < vend)) {
+                        mbar_wait_p(&b_empty[tail % UM_SLOTS], (tail / UM_SLOTS) & 1, pa, 0, pon);
+                        ++tail;
+                    }
+                    const uint32_t slot = seq % UM_SLOTS;
+                    const long long t_issue = pon ? clock64() : 0;
                     if (elect_one()) {
-                        const uint32_t bytes = ncols * 384u;
-                        mbar_expect_tx(&b_full[st], bytes);
-                        bulk_g2s(stage_base + (size_t)st * A.stage_bytes, A.bank + ((size_t)tt.y << 8), bytes,
-                                 &b_full[st]);
+                        s_vstart[slot] = v;
+                        mbar_expect_tx(&b_full[slot], bytes);
+                        bulk_g2s(stage_base + phys, A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * bytes, bytes,
+                                 &b_full[slot]);
                     }
                     __syncwarp();
-                    if (++st == (uint32_t)A.bstages) { st = 0; ph ^= 1; }
+                    if (pon) pa.c[1] += (unsigned long long)(clock64() - t_issue);
+                    vhead = vend;
+                    phys += bytes;
+                    ++seq;
                 }
             }
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer (whole warp, one elected lane) =============
-        uint32_t st = 0, ph = 0, wcnt = 0, acnt = 0;
+    } else if (warp == 1 && leader) {
+        // ===================== MMA issuer (leader CTA; whole warp, one elected lane) ==
+        uint32_t seq = 0, wcnt = 0, acnt = 0;
+        uint32_t phys = 0;  // ring offset: same allocation sequence as the producer
+        if (A.resident) {
+            mbar_wait_p(&b_full[0], 0, pa, 2, pon);  // the whole bank (both CTAs' halves)
+            tc_fence_after();
+        }
+        const uint32_t RING = A.ring_bytes;
         const uint32_t stage0 = smem_u32(stage_base);
-        for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x, ++wcnt) {
+        for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
             const uint32_t wb = wcnt % A.win_bufs;
+            WH_TRACE(0, wcnt);
             mbar_wait_p(&win_full[wb], (wcnt / A.win_bufs) & 1, pa, 0, pon);
             tc_fence_after();
-            const float e = wexp[wb];
+            WH_TRACE(1, wcnt);
             const uint32_t a_hi = smem_u32(win_base) + wb * 2 * WH;
             const uint32_t a_lo = a_hi + WH;
             for (int p = 0; p < A.n_passes; ++p, ++acnt) {
@@ -391,68 +569,93 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const uint32_t ab = acnt % A.n_acc;
                 mbar_wait_p(&acc_empty[ab], ((acnt / A.n_acc) & 1) ^ 1, pa, 1, pon);
                 tc_fence_after();
-                if (lane == 0) accexp[ab] = e;
                 const uint32_t d_acc = tmem + ab * (uint32_t)A.acc_stride;
-                uint32_t prev_c0 = (uint32_t)pinfo.w;  // pass columns
-                for (int t = pinfo.x; t < pinfo.y; ++t) {
-                    const uint2 tt = s_tile[t];
-                    const uint32_t k = tt.x & 0xffffu, c0 = (tt.x >> 16) & 0xffu, nc = tt.x >> 24;
-                    const uint32_t kg = k * 64u;
-                    const uint32_t aoff = ((kg % (uint32_t)A.V) >> 6) * panel_bytes + (kg / (uint32_t)A.V) * 128u;
-                    const uint32_t bt = stage0 + st * A.stage_bytes;  // [hi fwd | lo rev | hi rev]
-                    const uint32_t C = (uint32_t)pinfo.w;
-                    const bool first = (t == pinfo.x);
-                    const uint32_t nnew = first ? nc : (c0 < prev_c0 ? prev_c0 - c0 : 0u);
-                    mbar_wait_p(&b_full[st], ph, pa, 2, pon);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        // D columns of a pass: main_j at d + j (j = 0..C-1), corr_j at d + 2C-1-j.
-                        // MMA1: A_hi x [hi_c0..hi_C-1 | lo_C-1..lo_c0] -> [main_c0.. | ..corr_c0]
-                        // MMA2: A_lo x [hi_C-1..hi_c0]               -> [corr_C-1 .. corr_c0]
-                        const uint32_t d1 = d_acc + c0, d2 = d_acc + C;
-                        const uint32_t b2 = bt + 2 * nc * 128u;
-                        if (nnew == nc) {
-                            umma_f16(d1, sdesc(a_hi + aoff), sdesc(bt), idesc_f16(2 * nc), 0u);
-                        } else if (nnew > 0) {
-                            // first touch of columns [c0, c0+nnew): main head and corr tail
-                            umma_f16(d1, sdesc(a_hi + aoff), sdesc(bt), idesc_f16(nnew), 0u);
-                            umma_f16(d1 + nnew, sdesc(a_hi + aoff), sdesc(bt + nnew * 128u),
-                                     idesc_f16(2 * (nc - nnew)), 1u);
-                            umma_f16(d1 + 2 * nc - nnew, sdesc(a_hi + aoff), sdesc(bt + (2 * nc - nnew) * 128u),
-                                     idesc_f16(nnew), 0u);
-                        } else {
-                            umma_f16(d1, sdesc(a_hi + aoff), sdesc(bt), idesc_f16(2 * nc), 1u);
-                        }
-                        umma_f16(d2, sdesc(a_lo + aoff), sdesc(b2), idesc_f16(nc), 1u);
-#pragma unroll
-                        for (uint32_t j = 1; j < 4; ++j) {
-                            umma_f16(d1, sdesc(a_hi + aoff + j * 32), sdesc(bt + j * 32), idesc_f16(2 * nc), 1u);
-                            umma_f16(d2, sdesc(a_lo + aoff + j * 32), sdesc(b2 + j * 32), idesc_f16(nc), 1u);
-                        }
-                        umma_commit(&b_empty[st]);
+                const uint32_t C = (uint32_t)pinfo.w;
+                for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
+                    const int4 gr = s_group[gi];
+                    const uint32_t bytes = (uint32_t)gr.w;
+                    uint32_t gbase, slot = 0;
+                    if (A.resident) {
+                        gbase = stage0 + (uint32_t)s_goff[gi];
+                    } else {
+                        if (phys + bytes > RING) phys = 0;  // same ring allocation as the producer
+                        gbase = stage0 + phys;
+                        phys += bytes;
+                        slot = seq % UM_SLOTS;
+                        const uint32_t ph = (seq / UM_SLOTS) & 1;
+                        ++seq;
+                        mbar_wait_p(&b_full[slot], ph, pa, 2, pon);
+                        tc_fence_after();
                     }
-                    __syncwarp();
-                    if (c0 < prev_c0) prev_c0 = c0;
-                    if (++st == (uint32_t)A.bstages) { st = 0; ph ^= 1; }
+                    for (int t = gr.x; t < gr.y; ++t) {
+                        const uint2 tt = s_tile[t];
+                        const uint32_t c0 = (tt.x >> 16) & 0xffu, nc = tt.x >> 24;
+                        const uint32_t aoff = ((tt.x >> 12) & 0xfu) * panel_bytes + (tt.x & 0xfffu) * 128u;
+                        const uint32_t bt = gbase + tt.y;
+                        // MMA1: A_hi x [hi_c0..hi_C-1 | lo_C-1..lo_c0] -> main_j at col j, corr_j at 2C-1-j
+                        // MMA2: A_lo x [hi_C-1..hi_c0]               -> corr
+                        // (CG = 2: each CTA's stage holds half of every B operand)
+                        const uint32_t b2 = bt + (CG == 2 ? nc : 2 * nc) * 128u;
+                        const uint32_t d1 = d_acc + c0, d2 = d_acc + C;
+                        if (!(A.dbg & 4) && elect_one()) {
+#pragma unroll
+                            for (uint32_t j = 0; j < 4; ++j) {
+                                umma_f16<CG>(d1, sdesc(a_hi + aoff + j * 32), sdesc(bt + j * 32), idesc_f16<CG>(2 * nc));
+                                umma_f16<CG>(d2, sdesc(a_lo + aoff + j * 32), sdesc(b2 + j * 32), idesc_f16<CG>(nc));
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    if (!A.resident) {
+                        if (elect_one()) umma_commit<CG>(&b_empty[slot]);
+                        __syncwarp();
+                    }
                 }
-                if (elect_one()) umma_commit(&acc_full[ab]);
+                if (elect_one()) umma_commit<CG>(&acc_full[ab]);
                 __syncwarp();
             }
-            if (elect_one()) umma_commit(&win_empty[wb]);
+            if (elect_one()) umma_commit<CG>(&win_empty[wb]);
             __syncwarp();
+            WH_TRACE(2, wcnt);
+        }
+    } else if (warp == 1) {
+        // ===================== relay (peer CTA of a pair) ============================
+        // forwards "my window is converted" and "my half of the tap group landed" to the
+        // leader's barriers, which the leader's MMA issuer waits on.  (A non-tensor bulk copy
+        // completes on the destination CTA's own barrier -- tools/probe_remote_tx.cu.)
+        uint32_t wcnt = 0, seq = 0;
+        if (A.resident) {
+            mbar_wait_p(&b_full[0], 0, pa, 2, pon);
+            if (elect_one()) mbar_arrive_leader_relaxed(&b_full[0]);
+            __syncwarp();
+        }
+        for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
+            const uint32_t wb = wcnt % A.win_bufs;
+            mbar_wait_p(&win_full[wb], (wcnt / A.win_bufs) & 1, pa, 0, pon);
+            if (elect_one()) mbar_arrive_leader(&win_full[wb]);
+            __syncwarp();
+            for (int p = 0; p < (A.resident ? 0 : A.n_passes); ++p) {
+                const int4 pinfo = s_pass[p];
+                for (int gi = pinfo.x; gi < pinfo.y; ++gi, ++seq) {
+                    mbar_wait_p(&b_full[seq % UM_SLOTS], (seq / UM_SLOTS) & 1, pa, 2, pon);
+                    if (elect_one()) mbar_arrive_leader_relaxed(&b_full[seq % UM_SLOTS]);
+                    __syncwarp();
+                }
+            }
         }
     } else if (warp < 2 + UM_CONV_WARPS) {
         // ===================== converters ============================================
-        // The fp32 window of item i is a contiguous sample range of the clip; one elected
-        // converter thread bulk-copies it into the staging buffer one item ahead.
+        // The fp32 window of a tile is a contiguous sample range of the clip; one elected
+        // converter thread bulk-copies it into the staging buffer one unit ahead.
         const int ct = threadIdx.x - 64;  // 0 .. UM_CONV_THREADS-1
         const int cw = warp - 2;
         const int chunks = A.win_rows * A.panels * 8;  // 8-sample chunks in the window
         const int64_t wlen = (int64_t)A.win_rows * A.V;
-        float *stg = reinterpret_cast<float *>(stage_base + (size_t)A.bstages * A.stage_bytes);
+        float *stg = reinterpret_cast<float *>(stage_base + (size_t)A.ring_bytes);
         // staged range [lo, hi) of the clip for an item (16-byte granular); rest read directly
         auto staged = [&](int64_t item, int64_t &lo, int64_t &hi) {
-            const int64_t b = item / A.row_tiles, tile = item % A.row_tiles;
+            int64_t b, tile;
+            unit_tile(item, b, tile);
             const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
             lo = w0 > 0 ? w0 : 0;
             hi = w0 + wlen < A.N ? w0 + wlen : (A.N & ~(int64_t)3);
@@ -462,52 +665,62 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         auto issue = [&](int64_t item) {
             int64_t lo, hi;
             staged(item, lo, hi);
-            const int64_t b = item / A.row_tiles, tile = item % A.row_tiles;
+            int64_t b, tile;
+            unit_tile(item, b, tile);
             const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
             const uint32_t bytes = (uint32_t)((hi - lo) * 4);
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
-        if (A.use_stg && ct == 0 && (int64_t)blockIdx.x < A.items) issue(blockIdx.x);
+        if (A.use_stg && ct == 0 && u0 < n_units) issue(u0);
         uint32_t wcnt = 0;
-        for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x, ++wcnt) {
-            const int64_t b = item / A.row_tiles;
-            const int64_t tile = item % A.row_tiles;
+        for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
+            int64_t b, tile;
+            unit_tile(item, b, tile);
             const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
             const float *xb = A.x + b * A.ld_x;
             const uint32_t wb = wcnt % A.win_bufs;
             int64_t slo, shi;
             staged(item, slo, shi);
+            if (ct == 0) WH_TRACE(3, wcnt);
             if (A.use_stg) mbar_wait_p(&stg_full, wcnt & 1, pa, 0, pon);
-            // sample g of the window (clip index w0 + g): staged, direct (edge), or zero
-            auto load8 = [&](int row, int panel, int c8, float (&v)[8]) {
-                const int64_t off = (int64_t)row * A.V + panel * 64 + c8 * 8;
-                const int64_t g0 = w0 + off;
-                if (g0 >= slo && g0 + 8 <= shi) {
+            if (ct == 0) WH_TRACE(4, wcnt);
+            // chunk c = 8 consecutive samples: row = c >> cpr_shift, column chunk = c & cpr_mask
+            // (cpr = panels * 8 chunks per row); window offsets are 32-bit
+            const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
+            const int32_t st_lo = (int32_t)(slo - w0), st_hi = (int32_t)(shi - w0);  // staged range
+            const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);                       // clip start
+            const int64_t in_hi64 = A.N - w0;                                          // clip end
+            const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
+            auto load8 = [&](int32_t off, float (&v)[8]) {
+                if (off >= st_lo && off + 8 <= st_hi) {
                     const float4 u = *reinterpret_cast<const float4 *>(stg + off);
                     const float4 w = *reinterpret_cast<const float4 *>(stg + off + 4);
                     v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
-                } else if (A.vec_ok && g0 >= 0 && g0 + 8 <= A.N) {
-                    const float4 u = __ldg(reinterpret_cast<const float4 *>(xb + g0));
-                    const float4 w = __ldg(reinterpret_cast<const float4 *>(xb + g0) + 1);
+                } else if (A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
+                    const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
+                    const float4 u = __ldg(g), w = __ldg(g + 1);
                     v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
                 } else {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int64_t g = g0 + i;
-                        v[i] = (g >= 0 && g < A.N) ? ((g >= slo && g < shi) ? stg[off + i] : __ldg(xb + g)) : 0.0f;
+                        const int32_t o = off + i;
+                        v[i] = (o >= in_lo && o < in_hi) ? ((o >= st_lo && o < st_hi) ? stg[o] : __ldg(xb + w0 + o)) : 0.0f;
                     }
                 }
+            };
+            auto chunk_off = [&](int c) {
+                const int row = c >> cpr_shift, cc = c & cpr_mask;  // cc = panel * 8 + c8
+                return row * A.V + cc * 8;
             };
             // pass 1: max |x| over the window
             float mx = 0.0f;
 #pragma unroll 4
             for (int c = ct; c < chunks; c += UM_CONV_THREADS) {
-                const int row = c / (A.panels * 8), rem = c % (A.panels * 8);
                 float v[8];
-                load8(row, rem >> 3, rem & 7, v);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) mx = fmaxf(mx, fabsf(v[i]));
+                load8(chunk_off(c), v);
+                mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))),
+                                     fmaxf(fmaxf(fabsf(v[4]), fabsf(v[5])), fmaxf(fabsf(v[6]), fabsf(v[7])))));
             }
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
@@ -523,23 +736,26 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             }
             const float sc = ldexpf(1.0f, ex);
             // wait until the MMAs that read this window buffer win_bufs items ago are done
+            if (ct == 0) WH_TRACE(5, wcnt);
             mbar_wait_p(&win_empty[wb], ((wcnt / A.win_bufs) & 1) ^ 1, pa, 1, pon);
+            if (ct == 0) WH_TRACE(6, wcnt);
             uint8_t *whi = win_base + (size_t)wb * 2 * WH;
             uint8_t *wlo = whi + WH;
-            for (int c = ct; c < chunks; c += UM_CONV_THREADS) {
-                const int row = c / (A.panels * 8), rem = c % (A.panels * 8);
-                const int panel = rem >> 3, c8 = rem & 7;
+#pragma unroll 2
+            for (int c = ct; c < ((A.dbg & 2) ? 0 : chunks); c += UM_CONV_THREADS) {
+                const int row = c >> cpr_shift, cc = c & cpr_mask;
+                const int panel = cc >> 3, c8 = cc & 7;
                 float v[8];
-                load8(row, panel, c8, v);
+                load8(row * A.V + cc * 8, v);
                 uint32_t hw[4], lw[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const float a0 = v[2 * i] * sc, a1 = v[2 * i + 1] * sc;
-                    const __half h0 = __float2half_rn(a0), h1 = __float2half_rn(a1);
-                    const __half l0 = __float2half_rn(a0 - __half2float(h0));
-                    const __half l1 = __float2half_rn(a1 - __half2float(h1));
-                    hw[i] = pack_h2(h0, h1);
-                    lw[i] = pack_h2(l0, l1);
+                    const float2 a = make_float2(v[2 * i] * sc, v[2 * i + 1] * sc);
+                    const __half2 h = __float22half2_rn(a);            // hi = rn(x)
+                    const float2 hf = __half22float2(h);
+                    const __half2 l = __float22half2_rn(make_float2(a.x - hf.x, a.y - hf.y));  // lo = rn(x - hi)
+                    hw[i] = *reinterpret_cast<const uint32_t *>(&h);
+                    lw[i] = *reinterpret_cast<const uint32_t *>(&l);
                 }
                 const uint32_t off = (uint32_t)panel * panel_bytes + (uint32_t)row * 128u +
                                      (uint32_t)((c8 ^ (row & 7)) * 16);
@@ -547,24 +763,26 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 *reinterpret_cast<uint4 *>(wlo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (ct == 0) wexp[wb] = ldexpf(1.0f, -ex);
+            if (ct == 0) xring[wcnt & 3] = ldexpf(1.0f, -ex);
             asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
             // staging is free again: prefetch the next item's window
-            if (A.use_stg && ct == 0 && item + gridDim.x < A.items) issue(item + gridDim.x);
+            if (A.use_stg && ct == 0 && item + ustride < n_units) issue(item + ustride);
+            if (ct == 0) WH_TRACE(7, wcnt);
             if (lane == 0) mbar_arrive(&win_full[wb]);
         }
     } else {
         // ===================== epilogue ==============================================
         const int quad = warp & 3;          // TMEM lanes 32*quad .. 32*quad+31
+        const int half = (warp - 2 - UM_CONV_WARPS) >> 2;  // which 16-column units
         const int m = quad * 32 + lane;     // row within the tile
         const bool vec = A.out_vec_ok;
-        uint32_t acnt = 0;
+        uint32_t acnt = 0, ucnt = 0;
         float lmin = INFINITY, lmax = -INFINITY;
         int64_t cur_b = -1;
-        for (int64_t item = blockIdx.x; item < A.items; item += gridDim.x) {
-            const int64_t b = item / A.row_tiles;
-            const int64_t tile = item % A.row_tiles;
-            const int64_t mrow = tile * 128 + m;  // global row
+        for (int64_t item = u0; item < n_units; item += ustride, ++ucnt) {
+            int64_t b, tile;
+            unit_tile(item, b, tile);
+            const int64_t mrow = tile * 128 + m;  // global row (beyond rows_total: no frames)
             const int64_t frame0 = mrow * P;      // first frame of this row
             const int64_t rem_frames = A.F - frame0;
             const int nvalid = rem_frames <= 0 ? 0 : (rem_frames >= P ? P : (int)rem_frames);
@@ -587,34 +805,43 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             for (int p = 0; p < A.n_passes; ++p, ++acnt) {
                 const int4 pinfo = s_pass[p];
                 const uint32_t ab = acnt % A.n_acc;
+                if (warp == 2 + UM_CONV_WARPS && p == 0) WH_TRACE(8, ucnt);
                 mbar_wait_p(&acc_full[ab], (acnt / A.n_acc) & 1, pa, 0, pon);
                 tc_fence_after();
-                const float e = accexp[ab];
+                if (warp == 2 + UM_CONV_WARPS && p == 0) WH_TRACE(9, ucnt);
+                const float e = xring[ucnt & 3];
                 const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + ab * (uint32_t)A.acc_stride;
                 // corr_j lives at column 2C-1-j: the 16 corr values of unit u0 are loaded
                 // from cbase - u0 in reverse order
                 const uint32_t cbase = tbase + 2u * (uint32_t)pinfo.w - 16u;
                 const int s0 = pinfo.z & 0xffff, ns = pinfo.z >> 16;
-                switch (A.output) {
+                if (!(A.dbg & 1)) switch (A.output) {
                     case WH_OUT_COMPLEX64:
-                        epi_pass<CC, P, WH_OUT_COMPLEX64>(A, tbase, cbase, s0, ns, pinfo.w, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_COMPLEX64>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_ABS:
-                        epi_pass<CC, P, WH_OUT_ABS>(A, tbase, cbase, s0, ns, pinfo.w, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_ABS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_POWER:
-                        epi_pass<CC, P, WH_OUT_POWER>(A, tbase, cbase, s0, ns, pinfo.w, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_POWER>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_LOG_DB:
-                        epi_pass<CC, P, WH_OUT_LOG_DB>(A, tbase, cbase, s0, ns, pinfo.w, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_LOG_DB>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     default:
-                        epi_pass<CC, P, WH_OUT_LOG1P>(A, tbase, cbase, s0, ns, pinfo.w, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_LOG1P>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                 }
+                // the columns read were re-zeroed; release the buffer to the MMA issuer
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[ab]);
+                if (lane == 0) {
+                    // TMEM accesses are ordered by wait::st + fence::before_thread_sync; the
+                    // global stores need no ordering against the MMA: relaxed arrive
+                    if (CG == 2 && !leader) mbar_arrive_leader_relaxed(&acc_empty[ab]);
+                    else mbar_arrive(&acc_empty[ab]);
+                }
             }
         }
         if (A.minmax && cur_b >= 0) {
@@ -630,15 +857,18 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         }
     }
     if (pon && lane == 0) {
-        const int role = warp == 0 ? PR_PROD : warp == 1 ? PR_MMA : warp < 2 + UM_CONV_WARPS ? PR_CONV : PR_EPI;
+        const int role = warp == 0 ? PR_PROD : warp == 1 ? (leader ? PR_MMA : PR_RELAY) : warp < 2 + UM_CONV_WARPS ? PR_CONV : PR_EPI;
         prof_flush(pa, A.prof, role);
     }
     tc_fence_before();
-    __syncthreads();
+    cta_pair_sync<CG>();
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        if constexpr (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
@@ -653,7 +883,7 @@ struct BankArgs {
     const int64_t *half;
     const int32_t *fexp;
     double C, Bw;
-    int32_t P, Cc, G0;
+    int32_t P, Cc, G0, cg;
     int64_t hop;
     uint8_t *bank;
 };
@@ -667,9 +897,11 @@ __global__ void k_build_bank(BankArgs a) {
     const UmmaTile tl = a.tiles[t];
     const int CP = a.Cc * a.P;
     const int C = ps.cols;
-    uint8_t *part0 = a.bank + tl.byte_off;                 // hi, columns c0 .. C-1
-    uint8_t *part1 = part0 + (size_t)tl.ncols * 128;       // lo, columns C-1 .. c0
-    uint8_t *part2 = part1 + (size_t)tl.ncols * 128;       // hi, columns C-1 .. c0
+    // cg = 1: [hi fwd | lo rev | hi rev] (nc rows each, one CTA holds the whole tile)
+    // cg = 2: block of CTA 0 = [hi fwd | hi rev rows 0..nc/2), block of CTA 1 =
+    //         [lo rev | hi rev rows nc/2..nc) -- each CTA holds half of every MMA's B
+    uint8_t *tile0 = a.bank + tl.byte_off;
+    const int nc = tl.ncols;
     const double norm = pow(M_PI * a.Bw, -0.5);
     const double w = 2.0 * M_PI * a.C;
     for (int idx = threadIdx.x; idx < tl.ncols * 64; idx += blockDim.x) {
@@ -705,29 +937,40 @@ __global__ void k_build_bank(BankArgs a) {
             *reinterpret_cast<__half *>(base + off) = val;
         };
         const int rrev = C - 1 - col;  // row index in the reversed parts
-        put(part0, n, h);
-        put(part1, rrev, l);
-        put(part2, rrev, h);
+        if (a.cg == 2) {
+            uint8_t *blk0 = tile0, *blk1 = tile0 + tl.blk1_delta;
+            put(blk0, n, h);
+            put(blk1, rrev, l);
+            if (rrev < nc / 2) put(blk0, nc + rrev, h);
+            else put(blk1, nc + rrev - nc / 2, h);
+        } else {
+            put(tile0, n, h);
+            put(tile0 + (size_t)nc * 128, rrev, l);
+            put(tile0 + (size_t)nc * 256, rrev, h);
+        }
     }
 }
 
 using UmmaKernel = void (*)(const UmmaArgs);
 
-template <int CC>
+template <int CC, int CG>
 static UmmaKernel pick_p(int P) {
     switch (P) {
-        case 1: return k_umma<CC, 1>;
-        case 2: return k_umma<CC, 2>;
-        case 4: return k_umma<CC, 4>;
-        case 8: return k_umma<CC, 8>;
-        case 16: return k_umma<CC, 16>;
-        case 32: return k_umma<CC, 32>;
-        case 64: return k_umma<CC, 64>;
+        case 1: return k_umma<CC, 1, CG>;
+        case 2: return k_umma<CC, 2, CG>;
+        case 4: return k_umma<CC, 4, CG>;
+        case 8: return k_umma<CC, 8, CG>;
+        case 16: return k_umma<CC, 16, CG>;
+        case 32: return k_umma<CC, 32, CG>;
+        case 64: return k_umma<CC, 64, CG>;
         default: return nullptr;
     }
 }
 
-static UmmaKernel umma_kernel(int Cc, int P) { return Cc == 2 ? pick_p<2>(P) : pick_p<1>(P); }
+static UmmaKernel umma_kernel(int Cc, int P, int CG) {
+    if (CG == 2) return Cc == 2 ? pick_p<2, 2>(P) : pick_p<1, 2>(P);
+    return Cc == 2 ? pick_p<2, 1>(P) : pick_p<1, 1>(P);
+}
 
 int umma_supported(const Plan &p, std::string *why) {
     const int64_t H = p.hop;
@@ -761,9 +1004,9 @@ int umma_supported(const Plan &p, std::string *why) {
 // compact smem tile format: k < 2^16, c0 and ncols < 2^8, byte_off multiple of 256
 static int ncheck_tiles(const Plan &p) {
     for (auto &t : p.tiles)
-        if (t.k >= 65536 || t.c0 > 255 || t.ncols > 255 || (t.byte_off & 255) || (t.byte_off >> 8) >= (1LL << 32))
+        if ((int64_t)t.k * 64 / p.V >= 4096 || p.V / 64 > 16 || t.c0 > 255 || t.ncols > 255 || (t.byte_off & 127))
             return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table out of range");
-    if (16 * p.passes.size() + 8 * p.tiles.size() > 32 * 1024)
+    if (16 * p.passes.size() + 16 * p.groups_u.size() + 8 * p.tiles.size() + 4 * (size_t)p.S > 32 * 1024)
         return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table too large");
     return WH_OK;
 }
@@ -771,6 +1014,10 @@ static int ncheck_tiles(const Plan &p) {
 int umma_prepare(Plan &p) {
     const int64_t H = p.hop;
     p.V = (int32_t)(H <= 64 ? 64 : H);
+    if (const char *vm = std::getenv("WH_UMMA_VMUL")) {  // diagnostics: rows of V * vmul samples
+        const int vmul = std::atoi(vm);
+        if (vmul == 2 || vmul == 4) p.V = std::min<int32_t>(p.V * vmul, 256);
+    }
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
     p.panels = p.V / 64;
@@ -838,42 +1085,136 @@ int umma_prepare(Plan &p) {
             tl.k = k;
             tl.c0 = c0;
             tl.ncols = ps.cols - c0;
-            tl.byte_off = byte_off;
-            byte_off += (int64_t)tl.ncols * 384;  // [hi fwd | lo rev | hi rev], 128 B rows
             max_tile_cols = std::max(max_tile_cols, tl.ncols);
             p.tiles.push_back(tl);
         }
         ps.tile_end = (int32_t)p.tiles.size();
         if (ps.tile_end > ps.tile_begin) p.passes.push_back(ps);
     }
+    // CTA pairs (tcgen05 cta_group::2, M = 256): each CTA stages half of every tap tile
+    p.cg = (p.sms % 2 == 0 && std::getenv("WH_UMMA_CG1") == nullptr) ? 2 : 1;
+    // Group consecutive tiles of a pass into one bulk copy of up to group_target bytes per
+    // CTA: a copy costs ~250 issue cycles whatever its size (tools/probe_bulk.cu), so small
+    // tiles must travel together.  Bank layout per group: [CTA-0 blocks][CTA-1 blocks].
+    const int64_t tile_unit = p.cg == 2 ? 192 : 384;  // bytes per column per CTA
+    int64_t bank_cta = 0;
+    for (auto &t : p.tiles) bank_cta += tile_unit * t.ncols;
+    // budget known early: the opt-in smem minus static smem and slack (tables added below)
+    UmmaKernel kern0 = umma_kernel(p.Cc, p.P, p.cg);
+    if (!kern0) return fail(WH_E_UNSUPPORTED, "UMMA engine: unsupported phase count");
+    int optin0 = 0;
+    cudaDeviceGetAttribute(&optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device);
+    cudaFuncAttributes fa0{};
+    WH_CUDA_TRY(cudaFuncGetAttributes(&fa0, kern0));
+    const int64_t tables_est = 16 * (int64_t)p.passes.size() + 24 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S;
+    const int64_t budget0 = (int64_t)optin0 - (int64_t)fa0.sharedSizeBytes - 1024 - 64 - tables_est;
+    // Resident tap bank: when this CTA's share of the whole bank fits beside one window it
+    // is loaded once per kernel and never streamed (no per-K-step barriers at all).
+    p.resident = (bank_cta + win <= budget0 && std::getenv("WH_UMMA_NO_RESIDENT") == nullptr) ? 1 : 0;
+    int64_t group_target = p.resident ? 48 * 1024 : ((int64_t)p.tiles.size() >= 64 ? 48 * 1024 : 24 * 1024);
+    if (const char *g = std::getenv("WH_UMMA_GROUP_KB")) group_target = std::max(1, std::atoi(g)) * 1024;
+    p.groups_u.clear();
+    int64_t max_group = 0;
+    for (auto &ps : p.passes) {
+        ps.group_begin = (int32_t)p.groups_u.size();
+        int t = ps.tile_begin;
+        while (t < ps.tile_end) {
+            UmmaGroup gr{};
+            gr.tile_begin = t;
+            int64_t bytes = 0;
+            while (t < ps.tile_end && (bytes == 0 || bytes + tile_unit * p.tiles[t].ncols <= group_target)) {
+                p.tiles[t].in_off = (int32_t)bytes;
+                bytes += tile_unit * p.tiles[t].ncols;
+                ++t;
+            }
+            gr.tile_end = t;
+            gr.cta_bytes = (int32_t)bytes;
+            gr.bank_off = byte_off;
+            for (int i = gr.tile_begin; i < gr.tile_end; ++i) {
+                p.tiles[i].byte_off = byte_off + p.tiles[i].in_off;
+                p.tiles[i].blk1_delta = bytes;
+            }
+            byte_off += bytes * p.cg;
+            max_group = std::max(max_group, bytes);
+            p.groups_u.push_back(gr);
+        }
+        ps.group_end = (int32_t)p.groups_u.size();
+    }
     p.bank_bytes = byte_off;
-    const int64_t stage_bytes = (int64_t)max_tile_cols * 384;
-    const int64_t table_bytes = 16 * (int64_t)p.passes.size() + 8 * (int64_t)p.tiles.size();
-    const int64_t budget = UM_SMEM_BUDGET - table_bytes;
+    const int64_t stage_bytes = max_group;
+    const int64_t table_bytes = 16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
+                                8 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S;
+    // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
+    // alignment slack and the tables
+    UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
+    if (!kern) return fail(WH_E_UNSUPPORTED, "UMMA engine: unsupported phase count");
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device);
+    cudaFuncAttributes fa{};
+    WH_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+    const int64_t budget = (int64_t)optin - (int64_t)fa.sharedSizeBytes - 1024 - 64 - table_bytes;
     if (ncheck_tiles(p) != WH_OK) return WH_E_UNSUPPORTED;
-    // smem = window buffers (hi|lo fp16) [+ fp32 staging, same bytes as one window] + tap
-    // stages.  Preference: 2 windows + staging, 1 window + staging, 2 windows, 1 window.
+    // smem = window buffers (hi|lo fp16) [+ fp32 staging, same bytes as one window] + the
+    // tap-tile ring.  Long units (many K-steps per window) favour a deeper ring with one
+    // window; short units favour double-buffered windows.
+    const int64_t tiles_per_unit = (int64_t)p.tiles.size();
     int use_stg = 0;
-    {
-        const int opts[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
-        for (auto &o : opts) {
-            const int64_t fixed = (int64_t)(o[0] + o[1]) * win;
-            if (fixed + 2 * stage_bytes <= budget) {
+    int64_t ring = 0;
+    if (p.resident) {
+        // the "ring" is the whole resident bank; spend what is left on windows / staging
+        ring = (bank_cta + 1023) / 1024 * 1024;
+        const int opts_r[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
+        for (auto &o : opts_r)
+            if ((int64_t)(o[0] + o[1]) * win + ring <= budget) {
                 win_bufs = o[0];
                 use_stg = o[1];
-                bstages = (int)std::min<int64_t>(4, (budget - fixed) / stage_bytes);
+                break;
+            }
+        if (win_bufs == 0) p.resident = 0, ring = 0;
+    }
+    if (!p.resident) {
+        const int prefer_single = tiles_per_unit >= 64 && std::getenv("WH_UMMA_PREFER_DOUBLE") == nullptr;
+        const int opts_a[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
+        const int opts_b[4][2] = {{1, 1}, {2, 1}, {1, 0}, {2, 0}};
+        const int (*opts)[2] = prefer_single ? opts_b : opts_a;
+        const char *force = std::getenv("WH_UMMA_SMEM_OPT");  // diagnostics: force an option
+        const int ostart = force ? std::atoi(force) : 0;
+        for (int i = ostart; i < 4; ++i) {
+            const int64_t fixed = (int64_t)(opts[i][0] + opts[i][1]) * win;
+            const int64_t r = (budget - fixed) / 1024 * 1024;
+            if (r >= 3 * stage_bytes && r >= 64 * 1024) {
+                win_bufs = opts[i][0];
+                use_stg = opts[i][1];
+                ring = r;
                 break;
             }
         }
+        if (ring == 0) {  // last resort: one window, ring of at least two tiles
+            const int64_t r = (budget - win) / 1024 * 1024;
+            if (r >= 2 * stage_bytes) { win_bufs = 1; use_stg = 0; ring = r; }
+        }
     }
-    if (bstages < 2) return fail(WH_E_UNSUPPORTED, "UMMA engine: shared memory too small for 2 stages");
+    if (ring == 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: shared memory too small for the tap ring");
+    // smem offset of every group inside the ring when the bank is resident
+    {
+        int64_t off = 0;
+        for (auto &g : p.groups_u) {
+            g.pad_ = (int32_t)off;
+            off += g.cta_bytes;
+        }
+    }
+    bstages = (int)(ring / stage_bytes);
     p.win_bufs = win_bufs;
     p.bstages = bstages;
     p.use_stg = use_stg;
-    p.smem_bytes = (size_t)((win_bufs + use_stg) * win + bstages * stage_bytes) + 1024 + table_bytes;
+    p.ring_bytes = ring;
+    p.smem_bytes = (size_t)((win_bufs + use_stg) * win + ring) + 1024 + table_bytes;
 
     WH_CUDA_TRY(cudaMalloc(&p.d_passes, sizeof(UmmaPass) * p.passes.size()));
     WH_CUDA_TRY(cudaMalloc(&p.d_tiles, sizeof(UmmaTile) * p.tiles.size()));
+    WH_CUDA_TRY(cudaMalloc(&p.d_groups_u, sizeof(UmmaGroup) * p.groups_u.size()));
+    WH_CUDA_TRY(cudaMemcpy(p.d_groups_u, p.groups_u.data(), sizeof(UmmaGroup) * p.groups_u.size(),
+                           cudaMemcpyHostToDevice));
     WH_CUDA_TRY(cudaMalloc(&p.d_bank, (size_t)p.bank_bytes));
     WH_CUDA_TRY(cudaMalloc(&p.d_scale_pow, sizeof(float) * p.S));
     int32_t *d_fexp = nullptr;
@@ -885,13 +1226,12 @@ int umma_prepare(Plan &p) {
     BankArgs ba{};
     ba.passes = p.d_passes; ba.tiles = p.d_tiles; ba.n_passes = (int32_t)p.passes.size();
     ba.scales = p.d_scales; ba.half = p.d_half; ba.fexp = d_fexp; ba.C = p.C; ba.Bw = p.B;
-    ba.P = p.P; ba.Cc = p.Cc; ba.G0 = p.G0; ba.hop = p.hop; ba.bank = p.d_bank;
+    ba.P = p.P; ba.Cc = p.Cc; ba.G0 = p.G0; ba.hop = p.hop; ba.bank = p.d_bank; ba.cg = p.cg;
     k_build_bank<<<(unsigned)p.tiles.size(), 256>>>(ba);
+
     WH_CUDA_TRY(cudaGetLastError());
     WH_CUDA_TRY(cudaDeviceSynchronize());
     cudaFree(d_fexp);
-    UmmaKernel kern = umma_kernel(p.Cc, p.P);
-    if (!kern) return fail(WH_E_UNSUPPORTED, "UMMA engine: unsupported phase count");
     WH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
     return WH_OK;
 }
@@ -904,21 +1244,41 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.Qlo = p.Qlo; a.win_rows = p.win_rows; a.S = p.S;
     a.n_passes = (int32_t)p.passes.size(); a.n_tiles = (int32_t)p.tiles.size();
     a.wavelet = p.wavelet; a.output = p.output;
-    a.bstages = p.bstages; a.win_bufs = p.win_bufs; a.n_acc = p.n_acc; a.acc_stride = p.acc_stride;
+    a.win_bufs = p.win_bufs; a.n_acc = p.n_acc; a.acc_stride = p.acc_stride;
     a.use_stg = p.use_stg;
+    a.resident = p.resident;
+    a.cpr_shift = p.panels == 1 ? 3 : p.panels == 2 ? 4 : p.panels == 4 ? 5 : -1;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
-    a.passes = p.d_passes; a.tiles = p.d_tiles; a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
+    a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
     a.minmax = p.norm == WH_NORM_MINMAX ? p.d_minmax : nullptr;
     int max_cols = 16;
     for (auto &t : p.tiles) max_cols = std::max(max_cols, t.ncols);
-    a.stage_bytes = (uint32_t)max_cols * 384u;
+    a.clips = clips;
+    a.ring_bytes = (uint32_t)p.ring_bytes;
+    (void)max_cols;
     a.win_half_bytes = (uint32_t)p.panels * (uint32_t)p.win_rows * 128u;
-    const int64_t grid = std::min<int64_t>(a.items, p.sms);
     a.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (p.F % 4 == 0);
     a.prof = p.d_prof;
+    a.dbg = std::getenv("WH_UMMA_DBG") ? std::atoi(std::getenv("WH_UMMA_DBG")) : 0;
+    a.trace = p.d_trace;
+    const int64_t units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
+    int64_t grid = std::min<int64_t>(units * p.cg, p.sms);
+    if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
-    umma_kernel(p.Cc, p.P)<<<(unsigned)grid, UM_THREADS, p.smem_bytes, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(UM_THREADS);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.cg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    WH_CUDA_TRY(cudaLaunchKernelEx(&cfg, umma_kernel(p.Cc, p.P, p.cg), a));
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }

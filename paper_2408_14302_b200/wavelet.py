@@ -207,10 +207,16 @@ class CwthPlan:
     def profile(self, enable: bool = True):
         """Diagnostics: enable the UMMA kernel's per-role wait counters and return (and
         reset) the counters accumulated so far as {role: {wait slots, total}} cycles."""
-        buf = (ctypes.c_uint64 * 16)()
-        _lib.check(_lib.load().wh_plan_profile(self._h, int(enable), buf, 16))
-        roles = ("producer", "mma", "converter", "epilogue")
+        buf = (ctypes.c_uint64 * 20)()
+        _lib.check(_lib.load().wh_plan_profile(self._h, int(enable), buf, 20))
+        roles = ("producer", "mma", "converter", "epilogue", "relay")
         return {r: list(buf[i * 4:(i + 1) * 4]) for i, r in enumerate(roles)}
+
+    def trace(self, enable: bool = True):
+        """Diagnostics: CTA-0 timeline of the UMMA kernel, int64 [16 events, 32 units]."""
+        buf = (ctypes.c_int64 * (16 * 32))()
+        _lib.check(_lib.load().wh_plan_trace(self._h, int(enable), buf, 16 * 32))
+        return np.array(buf, dtype=np.int64).reshape(16, 32)
 
     # -- execution ------------------------------------------------------------------
     def _check_input(self, clips: int, n: int):

@@ -23,12 +23,15 @@ plan.profile(True)
 plan.execute(x, out)
 torch.cuda.synchronize()
 c = plan.profile(False)
-warps = {"producer": 1, "mma": 1, "converter": 4, "epilogue": 4}
-names = {"producer": ["b_empty", "-", "-"], "mma": ["win_full", "acc_empty", "b_full"],
-         "converter": ["stg_full", "win_empty", "-"], "epilogue": ["acc_full", "-", "-"]}
+warps = {"producer": 1, "mma": 0.5, "converter": 4, "epilogue": 8, "relay": 0.5}
+names = {"producer": ["b_empty", "issue", "-"], "mma": ["win_full", "acc_empty", "b_full"],
+         "converter": ["stg_full", "win_empty", "-"], "epilogue": ["acc_full", "-", "-"],
+         "relay": ["win_full", "-", "b_full"]}
 sms = min(148, clips * ((plan.frames + 127) // 128))
 for r, v in c.items():
     n = warps[r] * sms
+    if v[3] == 0:
+        continue
     tot = v[3] / n
     parts = ", ".join(f"{names[r][i]} {v[i] / n / tot * 100:5.1f}%" for i in range(3) if names[r][i] != "-")
     print(f"{w['name']} {r:9s} total {tot / 1e3:8.1f} kcyc  waits: {parts}")

@@ -1,0 +1,34 @@
+"""CTA-0 timeline of the UMMA kernel (diagnostics): per unit, when each role starts/ends."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2408_14302_b200 as wh  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--clips", type=int, default=0)
+a = ap.parse_args()
+w = bench.workload(a.config)
+clips = a.clips or (w["clips"] if w["scaling"] == "weak" else 148)
+x = torch.from_numpy(bench.make_inputs(w, clips, 0)).cuda()
+plan = wh.CwthPlan(w["scales"], wh.MorletParams(), w["hop"], w["n"], wavelet=w["wavelet"],
+                   output=w["output"], norm=w["norm"], max_clips=clips, engine="umma")
+out = plan.execute(x)
+plan.trace(True)
+plan.execute(x, out)
+torch.cuda.synchronize()
+t = plan.trace(False)
+t0 = t[t > 0].min()
+names = ["mma_wait_win", "mma_start", "mma_end", "cv_wait_stg", "cv_stg_ok", "cv_wait_wempty", "cv_wempty_ok",
+         "cv_done", "epi_wait", "epi_start", "epi_end"]
+print("unit " + " ".join(f"{n:>13s}" for n in names) + "   (kcycles from first event)")
+for u in range(12):
+    if t[1, u] == 0:
+        break
+    print(f"{u:4d} " + " ".join(f"{(t[e, u] - t0) / 1e3:13.1f}" for e in range(len(names))))
