@@ -52,6 +52,7 @@ struct UmmaArgs {
     int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
     int32_t resident;                   // the whole tap bank lives in the ring (loaded once)
     int32_t cpr_shift;                  // log2(8-sample chunks per window row) = log2(panels * 8)
+    int32_t conv_regs;                  // converters prefetch the window into registers
     const UmmaPass *passes;
     const UmmaTile *tiles;
     const UmmaGroup *groups;
@@ -632,7 +633,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
             const uint32_t wb = wcnt % A.win_bufs;
             mbar_wait_p(&win_full[wb], (wcnt / A.win_bufs) & 1, pa, 0, pon);
-            if (elect_one()) mbar_arrive_leader(&win_full[wb]);
+            if (elect_one()) {
+                if (A.dbg & 8) mbar_arrive_leader_relaxed(&win_full[wb]);  // diagnostics only
+                else mbar_arrive_leader(&win_full[wb]);
+            }
             __syncwarp();
             for (int p = 0; p < (A.resident ? 0 : A.n_passes); ++p) {
                 const int4 pinfo = s_pass[p];
@@ -672,6 +676,93 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
+        if (A.conv_regs) {
+            // Register-prefetch path (no staging buffer): each thread loads its <= CONV_RC
+            // chunks of the next window into registers while the MMAs of the previous unit
+            // run, then converts from registers once the window buffer is free.
+            constexpr int CONV_RC = 10;
+            const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
+            uint32_t wcnt = 0;
+            for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
+                int64_t b, tile;
+                unit_tile(item, b, tile);
+                const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
+                const float *xb = A.x + b * A.ld_x;
+                const uint32_t wb = wcnt % A.win_bufs;
+                const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);
+                const int64_t in_hi64 = A.N - w0;
+                const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
+                if (ct == 0) WH_TRACE(3, wcnt);
+                float v[CONV_RC][8];
+                float mx = 0.0f;
+#pragma unroll
+                for (int i = 0; i < CONV_RC; ++i) {
+                    const int c = ct + i * UM_CONV_THREADS;
+                    const int32_t off = (c >> cpr_shift) * A.V + (c & cpr_mask) * 8;
+                    if (c < chunks && A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
+                        const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
+                        const float4 u = __ldg(g), w = __ldg(g + 1);
+                        v[i][0] = u.x; v[i][1] = u.y; v[i][2] = u.z; v[i][3] = u.w;
+                        v[i][4] = w.x; v[i][5] = w.y; v[i][6] = w.z; v[i][7] = w.w;
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int32_t o = off + k;
+                            v[i][k] = (c < chunks && o >= in_lo && o < in_hi) ? __ldg(xb + w0 + o) : 0.0f;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < CONV_RC; ++i)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(v[i][k]));
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+                if (lane == 0) red[cw] = mx;
+                asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
+                mx = red[0];
+#pragma unroll
+                for (int i = 1; i < UM_CONV_WARPS; ++i) mx = fmaxf(mx, red[i]);
+                int ex = 0;
+                if (mx > 0.0f) {
+                    frexpf(mx, &ex);
+                    ex = 14 - ex;
+                }
+                const float sc = ldexpf(1.0f, ex);
+                if (ct == 0) WH_TRACE(5, wcnt);
+                mbar_wait_p(&win_empty[wb], ((wcnt / A.win_bufs) & 1) ^ 1, pa, 1, pon);
+                if (ct == 0) WH_TRACE(6, wcnt);
+                uint8_t *whi = win_base + (size_t)wb * 2 * WH;
+                uint8_t *wlo = whi + WH;
+#pragma unroll
+                for (int i = 0; i < CONV_RC; ++i) {
+                    const int c = ct + i * UM_CONV_THREADS;
+                    if (c < chunks) {
+                        const int row = c >> cpr_shift, cc = c & cpr_mask;
+                        const int panel = cc >> 3, c8 = cc & 7;
+                        uint32_t hw[4], lw[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 a = make_float2(v[i][2 * k] * sc, v[i][2 * k + 1] * sc);
+                            const __half2 h = __float22half2_rn(a);
+                            const float2 hf = __half22float2(h);
+                            const __half2 l = __float22half2_rn(make_float2(a.x - hf.x, a.y - hf.y));
+                            hw[k] = *reinterpret_cast<const uint32_t *>(&h);
+                            lw[k] = *reinterpret_cast<const uint32_t *>(&l);
+                        }
+                        const uint32_t off = (uint32_t)panel * panel_bytes + (uint32_t)row * 128u +
+                                             (uint32_t)((c8 ^ (row & 7)) * 16);
+                        *reinterpret_cast<uint4 *>(whi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        *reinterpret_cast<uint4 *>(wlo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (ct == 0) xring[wcnt & 3] = ldexpf(1.0f, -ex);
+                asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
+                if (ct == 0) WH_TRACE(7, wcnt);
+                if (lane == 0) mbar_arrive(&win_full[wb]);
+            }
+        } else {
         if (A.use_stg && ct == 0 && u0 < n_units) issue(u0);
         uint32_t wcnt = 0;
         for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
@@ -769,6 +860,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             if (A.use_stg && ct == 0 && item + ustride < n_units) issue(item + ustride);
             if (ct == 0) WH_TRACE(7, wcnt);
             if (lane == 0) mbar_arrive(&win_full[wb]);
+        }
         }
     } else {
         // ===================== epilogue ==============================================
@@ -1248,6 +1340,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.use_stg = p.use_stg;
     a.resident = p.resident;
     a.cpr_shift = p.panels == 1 ? 3 : p.panels == 2 ? 4 : p.panels == 4 ? 5 : -1;
+    a.conv_regs = (!p.use_stg && (int64_t)p.win_rows * p.panels * 8 <= 10 * 128 && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
