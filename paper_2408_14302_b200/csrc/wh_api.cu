@@ -110,18 +110,19 @@ __global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip,
         base[i] = constant ? 0.0f : (base[i] - lo) * sc;
 }
 
-int minmax_reset(Plan &p, int64_t clips, cudaStream_t s) {
-    k_minmax_reset<<<(unsigned)((clips + 255) / 256), 256, 0, s>>>(p.d_minmax, clips);
+int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, cudaStream_t s) {
+    (void)p;
+    k_minmax_reset<<<(unsigned)((clips + 255) / 256), 256, 0, s>>>(mm, clips);
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }
 
-int minmax_apply(Plan &p, int64_t clips, void *out, cudaStream_t s) {
+int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s) {
     int64_t per_clip = (int64_t)p.S * p.F;
     int vec = (per_clip % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
     int64_t work = vec ? per_clip / 4 : per_clip;
     unsigned bx = (unsigned)std::min<int64_t>(std::max<int64_t>((work + 1023) / 1024, 1), 64);
-    k_minmax_apply<<<dim3(bx, (unsigned)clips), 256, 0, s>>>((float *)out, p.d_minmax, per_clip, vec);
+    k_minmax_apply<<<dim3(bx, (unsigned)clips), 256, 0, s>>>((float *)out, mm, per_clip, vec);
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }
@@ -198,6 +199,7 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow);
     cudaFree(p->d_minmax); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->stream2) cudaStreamDestroy(p->stream2);
     cudaSetDevice(cur);
     delete p;
 }
@@ -281,7 +283,8 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
             }
         }
     }
-    if (rc == WH_OK && cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (rc == WH_OK && (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+                        cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess))
         rc = fail(WH_E_CUDA, "cudaStreamCreate failed");
     if (rc == WH_OK && cudaDeviceSynchronize() != cudaSuccess)
         rc = fail(WH_E_CUDA, std::string("plan build failed: ") + cudaGetErrorString(cudaGetLastError()));
@@ -353,6 +356,17 @@ int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im,
     return WH_OK;
 }
 
+static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev, cudaStream_t s,
+                        uint32_t *mm) {
+    int rc = WH_OK;
+    if (p->norm == WH_NORM_MINMAX) rc = minmax_reset(*p, clips, mm, s);
+    if (rc == WH_OK)
+        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, out_dev, s, mm)
+                                           : simt_launch(*p, x_dev, clips, ld_x, out_dev, s, mm);
+    if (rc == WH_OK && p->norm == WH_NORM_MINMAX) rc = minmax_apply(*p, clips, out_dev, mm, s);
+    return rc;
+}
+
 int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev,
                void *stream) {
     if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
@@ -365,14 +379,18 @@ int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, v
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != p->device) WH_CUDA_TRY(cudaSetDevice(p->device));
-    int rc = WH_OK;
-    if (p->norm == WH_NORM_MINMAX) rc = minmax_reset(*p, clips, s);
-    if (rc == WH_OK)
-        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, out_dev, s)
-                                           : simt_launch(*p, x_dev, clips, ld_x, out_dev, s);
-    if (rc == WH_OK && p->norm == WH_NORM_MINMAX) rc = minmax_apply(*p, clips, out_dev, s);
+    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax);
     if (prev != p->device) cudaSetDevice(prev);
     return rc;
+}
+
+static bool is_pinned(const void *ptr) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
 }
 
 int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out_host) {
@@ -400,16 +418,34 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
         WH_CUDA_TRY(cudaMalloc(&p->d_out, cap));
         p->d_out_bytes = cap;
     }
-    WH_CUDA_TRY(cudaMemcpyAsync(p->d_x, x_host, xb, cudaMemcpyHostToDevice, p->stream));
-    int rc = wh_execute(plan, p->d_x, clips, p->N, p->d_out, p->stream);
-    if (rc != WH_OK) {
-        cudaSetDevice(prev);
-        return rc;
+    // Pinned host buffers: pipeline clip chunks over two streams so that the H2D copy of
+    // chunk j+1, the kernel of chunk j and the D2H copy of chunk j-1 overlap (PCIe is full
+    // duplex).  Pageable buffers: one chunk (the copies are staged by the driver anyway).
+    const bool pinned = is_pinned(x_host) && is_pinned(out_host);
+    const int64_t n_chunks = (pinned && clips >= 4) ? std::min<int64_t>(8, clips) : 1;
+    const int64_t per = (clips + n_chunks - 1) / n_chunks;
+    const size_t out_clip = (size_t)p->S * p->F * out_elem_bytes(*p);
+    int rc = WH_OK;
+    for (int64_t c0 = 0, j = 0; c0 < clips && rc == WH_OK; c0 += per, ++j) {
+        const int64_t nc = std::min(per, clips - c0);
+        cudaStream_t s = (j & 1) ? p->stream2 : p->stream;
+        float *dx = p->d_x + (size_t)c0 * p->N;
+        uint8_t *dout = reinterpret_cast<uint8_t *>(p->d_out) + (size_t)c0 * out_clip;
+        if (cudaMemcpyAsync(dx, x_host + (size_t)c0 * p->N, sizeof(float) * (size_t)nc * p->N,
+                            cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            rc = fail(WH_E_CUDA, "H2D copy failed");
+            break;
+        }
+        rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0);
+        if (rc == WH_OK && cudaMemcpyAsync(reinterpret_cast<uint8_t *>(out_host) + (size_t)c0 * out_clip, dout,
+                                           (size_t)nc * out_clip, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            rc = fail(WH_E_CUDA, "D2H copy failed");
     }
-    WH_CUDA_TRY(cudaMemcpyAsync(out_host, p->d_out, ob, cudaMemcpyDeviceToHost, p->stream));
-    WH_CUDA_TRY(cudaStreamSynchronize(p->stream));
+    const cudaError_t e1 = cudaStreamSynchronize(p->stream), e2 = cudaStreamSynchronize(p->stream2);
+    if (rc == WH_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
+        rc = fail(WH_E_CUDA, std::string("execute_host failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
     cudaSetDevice(prev);
-    return WH_OK;
+    return rc;
 }
 
 int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n) {

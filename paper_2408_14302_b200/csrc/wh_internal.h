@@ -118,7 +118,7 @@ struct Plan {
     float *d_x = nullptr;
     void *d_out = nullptr;
     size_t d_x_bytes = 0, d_out_bytes = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, stream2 = nullptr;  // wh_execute_host pipeline
 };
 
 int64_t out_elem_bytes(const Plan &p);
@@ -128,14 +128,14 @@ int build_fold_bank(Plan &p);
 
 // engines
 int simt_prepare(Plan &p);
-int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s);
+int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm);
 int umma_supported(const Plan &p, std::string *why);
 int umma_prepare(Plan &p);
-int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s);
+int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm);
 
 // epilogue helpers (wh_api.cu)
-int minmax_reset(Plan &p, int64_t clips, cudaStream_t s);
-int minmax_apply(Plan &p, int64_t clips, void *out, cudaStream_t s);
+int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, cudaStream_t s);
+int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s);
 
 }  // namespace wh
 

@@ -1,3 +1,3 @@
-timeout 60 python tools/gpu_check.py umma 2>&1 | grep -v FAILED | cut -c1-80 | tail -14
-for c in c2 c1 c3 c4h16 c4h64 c4h256 c5; do timeout 45 python tools/prof_roles.py --config $c $([ $c = c5 ] && echo --clips 148); done
-for c in c2 c1 c3 c4h16 c4h64 c4h256 c5; do timeout 90 python bench.py --config $c --clips $([ $c = c5 ] && echo 296 || echo 0) --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], d['config']['engine'], '%.3e coeffs/s' % d['value'], '%.4f ms' % d['ms_per_step'], 'frac %.3f' % d['roofline']['frac'], d['clocks']['sm_mhz'])"; done
+set -x
+timeout 400 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 180 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -1
