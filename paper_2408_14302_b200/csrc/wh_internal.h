@@ -105,7 +105,9 @@ struct Plan {
     int32_t n_acc = 2, acc_stride = 256;   // TMEM accumulator buffers, columns per buffer
     int32_t use_stg = 1;                   // fp32 window staged by cp.async.bulk
     int32_t cg = 2;                        // CTAs per MMA (tcgen05 cta_group)
-    int32_t resident = 0;                  // whole tap bank resident in smem
+    int32_t resident = 0;                  // (part of) the tap bank resident in smem
+    int64_t res_bytes = 0;                 // resident bytes per CTA (the stage region's prefix)
+    int32_t n_stream = 0;                  // tap groups streamed through the ring per unit
     size_t smem_bytes = 0;     // dynamic shared memory of the engine kernel
 
     unsigned long long *d_prof = nullptr;  // diagnostics counters (wh_plan_profile)

@@ -50,7 +50,9 @@ struct UmmaArgs {
     int32_t n_passes, n_tiles, wavelet, output, win_bufs, vec_ok;
     int32_t n_acc, acc_stride;          // accumulator buffers; columns per buffer (main|corr)
     int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
-    int32_t resident;                   // the whole tap bank lives in the ring (loaded once)
+    int32_t resident;                   // some tap groups live in smem for the whole kernel
+    uint32_t res_bytes;                 // bytes of the resident region at the stage base
+    int32_t n_stream;                   // tap groups streamed through the ring every unit
     int32_t cpr_shift;                  // log2(8-sample chunks per window row) = log2(panels * 8)
     int32_t conv_regs;                  // converters prefetch the window into registers
     const UmmaPass *passes;
@@ -146,10 +148,8 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // K-major, 128B-swizzle smem matrix descriptor (SBO = 8 rows * 128 B).
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
-    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
-           ((uint64_t)2 << 61);
-}
+// high word of every smem descriptor: SBO = 1024 B (8-row atoms), version 1, 128 B swizzle
+static constexpr uint64_t DESC_HI = ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
     asm volatile(
@@ -181,6 +181,15 @@ __device__ __forceinline__ void mbar_arrive_leader_relaxed(uint64_t *b) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(b)));
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// arrive on the leader's barrier after this CTA's own shared-memory writes: release at CTA
+// scope (MEMBAR.CTA) -- the writes target this CTA's shared memory, which the pair's MMA
+// reads in place, so they are performed once they are ordered at CTA scope.  The cluster-
+// scope release (MEMBAR.GPU, ~1k cycles) is kept for diagnostics (WH_UMMA_DBG & 8).
+__device__ __forceinline__ void mbar_arrive_leader_cta(uint64_t *b) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(b)));
+    asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // arrive on the barrier at the same smem offset in the leader CTA (rank 0) of the pair
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t *b) {
@@ -396,13 +405,15 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
 template <int CC, int P, int CG>
 __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ UmmaArgs A) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1 KB aligned (128 B swizzle atoms); pointer arithmetic on the shared array (not an
+    // integer round trip) keeps the shared address space visible to the compiler: LDS/STS
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t b_full[UM_SLOTS], b_empty[UM_SLOTS];
     __shared__ uint64_t s_vstart[UM_SLOTS];  // producer-private: ring start of in-flight slots
     __shared__ __align__(8) uint64_t win_full[2], win_empty[2], acc_full[2], acc_empty[2];
     __shared__ float xring[4];  // per-unit window exponent 2^-e, written by the converters
     __shared__ float red[UM_CONV_WARPS];
-    __shared__ __align__(8) uint64_t stg_full;
+    __shared__ __align__(8) uint64_t stg_full, res_full;
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -426,7 +437,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     int4 *s_pass = reinterpret_cast<int4 *>(stage_base + (size_t)A.ring_bytes +
                                             (A.use_stg ? 2 * (size_t)WH : 0));
     int4 *s_group = s_pass + A.n_passes;
-    uint2 *s_tile = reinterpret_cast<uint2 *>(s_group + A.n_groups);
+    uint4 *s_tile = reinterpret_cast<uint4 *>(s_group + A.n_groups);
     int *s_goff = reinterpret_cast<int *>(s_tile + A.n_tiles);  // resident: smem offset per group
     float *s_spow = reinterpret_cast<float *>(s_goff + A.n_groups);
     for (int i = threadIdx.x; i < A.S; i += blockDim.x) s_spow[i] = A.scale_pow[i];
@@ -443,8 +454,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const UmmaTile tl = A.tiles[i];
         // window row shift q and panel of this K-step's A operand (k*64 = q*V + panel*64)
         const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)A.V, panel = (kg % (uint32_t)A.V) >> 6;
-        s_tile[i] = make_uint2(q | (panel << 12) | ((uint32_t)tl.c0 << 16) | ((uint32_t)tl.ncols << 24),
-                               (uint32_t)tl.in_off);
+        // pre-decoded MMA operands of the K-step, in 16-byte descriptor units:
+        //   x = A offset in the window | c0 << 16,   y = B offset in the group | B2 delta << 16,
+        //   z = instruction descriptor of MMA1 (N = 2nc), w = of MMA2 (N = nc)
+        const uint32_t aoff = panel * (uint32_t)A.win_rows * 128u + q * 128u;
+        const uint32_t nc = (uint32_t)tl.ncols;
+        const uint32_t b2d = (CG == 2 ? nc : 2 * nc) * 128u;
+        s_tile[i] = make_uint4((aoff >> 4) | ((uint32_t)tl.c0 << 16), ((uint32_t)tl.in_off >> 4) | ((b2d >> 4) << 16),
+                               idesc_f16<CG>(2 * nc), idesc_f16<CG>(nc));
     }
 
     if (threadIdx.x == 0) {
@@ -453,12 +470,13 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_init(&b_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&win_full[i], UM_CONV_WARPS + ((CG == 2 && leader) ? 1 : 0));
+            mbar_init(&win_full[i], (CG == 2 && leader) ? 2 : 1);  // + the peer's converters
             mbar_init(&win_empty[i], 1);
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], UM_EPI_WARPS * CG);  // epilogue warps of both CTAs (leader's copy)
         }
         mbar_init(&stg_full, 1);
+        mbar_init(&res_full, (CG == 2 && leader) ? 2 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -498,27 +516,33 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         // straddles the physical end, and a slot is reused once the MMAs that read the
         // oldest bytes in the way have committed.
         if (A.resident) {
-            // one barrier for the whole bank: arm it with all bytes, then copy every group
+            // one barrier for the resident groups: arm it with all bytes, then copy them
             if (elect_one()) {
                 uint32_t total = 0;
-                for (int gi = 0; gi < A.n_groups; ++gi) total += (uint32_t)s_group[gi].w;
-                mbar_expect_tx(&b_full[0], total);
+                for (int gi = 0; gi < A.n_groups; ++gi)
+                    if (s_goff[gi] >= 0) total += (uint32_t)s_group[gi].w;
+                mbar_expect_tx(&res_full, total);
                 for (int gi = 0; gi < A.n_groups; ++gi) {
                     const int4 gr = s_group[gi];
-                    bulk_g2s(stage_base + s_goff[gi], A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * gr.w,
-                             (uint32_t)gr.w, &b_full[0]);
+                    if (s_goff[gi] >= 0)
+                        bulk_g2s(stage_base + s_goff[gi], A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * gr.w,
+                                 (uint32_t)gr.w, &res_full);
                 }
             }
             __syncwarp();
         }
+        // streamed groups (all of them without a resident region, the tail K-steps of a
+        // unit in hybrid mode) cycle through the ring that follows the resident region
+        uint8_t *ring_base = stage_base + A.res_bytes;
         uint64_t vhead = 0;   // virtual (monotonic) ring offset
         uint32_t phys = 0;    // vhead % RING, tracked incrementally
         uint32_t seq = 0, tail = 0;
-        const uint32_t RING = A.ring_bytes;
-        for (int64_t item = A.resident ? n_units : u0; item < n_units; item += ustride) {
+        const uint32_t RING = A.ring_bytes - A.res_bytes;
+        for (int64_t item = A.n_stream ? u0 : n_units; item < n_units; item += ustride) {
             for (int p = 0; p < A.n_passes; ++p) {
                 const int4 pinfo = s_pass[p];
                 for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
+                    if (s_goff[gi] >= 0) continue;  // resident
                     const int4 gr = s_group[gi];
                     const uint32_t bytes = (uint32_t)gr.w;
                     uint64_t v = vhead;
@@ -536,7 +560,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     if (elect_one()) {
                         s_vstart[slot] = v;
                         mbar_expect_tx(&b_full[slot], bytes);
-                        bulk_g2s(stage_base + phys, A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * bytes, bytes,
+                        bulk_g2s(ring_base + phys, A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * bytes, bytes,
                                  &b_full[slot]);
                     }
                     __syncwarp();
@@ -552,19 +576,18 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         uint32_t seq = 0, wcnt = 0, acnt = 0;
         uint32_t phys = 0;  // ring offset: same allocation sequence as the producer
         if (A.resident) {
-            mbar_wait_p(&b_full[0], 0, pa, 2, pon);  // the whole bank (both CTAs' halves)
+            mbar_wait_p(&res_full, 0, pa, 2, pon);  // the resident groups (both CTAs' halves)
             tc_fence_after();
         }
-        const uint32_t RING = A.ring_bytes;
-        const uint32_t stage0 = smem_u32(stage_base);
+        const uint32_t RING = A.ring_bytes - A.res_bytes;
+        const uint32_t stage0 = smem_u32(stage_base), ring0 = stage0 + A.res_bytes;
         for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
             const uint32_t wb = wcnt % A.win_bufs;
             WH_TRACE(0, wcnt);
             mbar_wait_p(&win_full[wb], (wcnt / A.win_bufs) & 1, pa, 0, pon);
             tc_fence_after();
             WH_TRACE(1, wcnt);
-            const uint32_t a_hi = smem_u32(win_base) + wb * 2 * WH;
-            const uint32_t a_lo = a_hi + WH;
+            const uint32_t a_hi16 = (smem_u32(win_base) + wb * 2 * WH) >> 4, wh16 = WH >> 4;
             for (int p = 0; p < A.n_passes; ++p, ++acnt) {
                 const int4 pinfo = s_pass[p];
                 const uint32_t ab = acnt % A.n_acc;
@@ -576,11 +599,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     const int4 gr = s_group[gi];
                     const uint32_t bytes = (uint32_t)gr.w;
                     uint32_t gbase, slot = 0;
-                    if (A.resident) {
-                        gbase = stage0 + (uint32_t)s_goff[gi];
+                    const int goff = s_goff[gi];
+                    if (goff >= 0) {
+                        gbase = stage0 + (uint32_t)goff;
                     } else {
                         if (phys + bytes > RING) phys = 0;  // same ring allocation as the producer
-                        gbase = stage0 + phys;
+                        gbase = ring0 + phys;
                         phys += bytes;
                         slot = seq % UM_SLOTS;
                         const uint32_t ph = (seq / UM_SLOTS) & 1;
@@ -588,26 +612,26 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         mbar_wait_p(&b_full[slot], ph, pa, 2, pon);
                         tc_fence_after();
                     }
+                    const uint32_t g16 = gbase >> 4;
                     for (int t = gr.x; t < gr.y; ++t) {
-                        const uint2 tt = s_tile[t];
-                        const uint32_t c0 = (tt.x >> 16) & 0xffu, nc = tt.x >> 24;
-                        const uint32_t aoff = ((tt.x >> 12) & 0xfu) * panel_bytes + (tt.x & 0xfffu) * 128u;
-                        const uint32_t bt = gbase + tt.y;
                         // MMA1: A_hi x [hi_c0..hi_C-1 | lo_C-1..lo_c0] -> main_j at col j, corr_j at 2C-1-j
                         // MMA2: A_lo x [hi_C-1..hi_c0]               -> corr
-                        // (CG = 2: each CTA's stage holds half of every B operand)
-                        const uint32_t b2 = bt + (CG == 2 ? nc : 2 * nc) * 128u;
-                        const uint32_t d1 = d_acc + c0, d2 = d_acc + C;
+                        // (CG = 2: each CTA's stage holds half of every B operand).  Descriptor
+                        // low words are 16-byte smem addresses (< 2^14): no masking needed.
+                        const uint4 tt = s_tile[t];
+                        const uint32_t ah = a_hi16 + (tt.x & 0xffffu), al = ah + wh16;
+                        const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
+                        const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
                         if (!(A.dbg & 4) && elect_one()) {
 #pragma unroll
                             for (uint32_t j = 0; j < 4; ++j) {
-                                umma_f16<CG>(d1, sdesc(a_hi + aoff + j * 32), sdesc(bt + j * 32), idesc_f16<CG>(2 * nc));
-                                umma_f16<CG>(d2, sdesc(a_lo + aoff + j * 32), sdesc(b2 + j * 32), idesc_f16<CG>(nc));
+                                umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                                umma_f16<CG>(d2, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
                             }
                         }
                         __syncwarp();
                     }
-                    if (!A.resident) {
+                    if (goff < 0) {
                         if (elect_one()) umma_commit<CG>(&b_empty[slot]);
                         __syncwarp();
                     }
@@ -621,29 +645,24 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ===================== relay (peer CTA of a pair) ============================
-        // forwards "my window is converted" and "my half of the tap group landed" to the
-        // leader's barriers, which the leader's MMA issuer waits on.  (A non-tensor bulk copy
-        // completes on the destination CTA's own barrier -- tools/probe_remote_tx.cu.)
-        uint32_t wcnt = 0, seq = 0;
+        // forwards "my half of the tap group landed" to the leader's barriers, which the
+        // leader's MMA issuer waits on.  (A non-tensor bulk copy completes on the destination
+        // CTA's own barrier -- tools/probe_remote_tx.cu.)
+        uint32_t seq = 0;
         if (A.resident) {
-            mbar_wait_p(&b_full[0], 0, pa, 2, pon);
-            if (elect_one()) mbar_arrive_leader_relaxed(&b_full[0]);
+            mbar_wait_p(&res_full, 0, pa, 2, pon);
+            if (elect_one()) mbar_arrive_leader_relaxed(&res_full);
             __syncwarp();
         }
-        for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
-            const uint32_t wb = wcnt % A.win_bufs;
-            mbar_wait_p(&win_full[wb], (wcnt / A.win_bufs) & 1, pa, 0, pon);
-            if (elect_one()) {
-                if (A.dbg & 8) mbar_arrive_leader_relaxed(&win_full[wb]);  // diagnostics only
-                else mbar_arrive_leader(&win_full[wb]);
-            }
-            __syncwarp();
-            for (int p = 0; p < (A.resident ? 0 : A.n_passes); ++p) {
+        for (int64_t item = A.n_stream ? u0 : n_units; item < n_units; item += ustride) {
+            for (int p = 0; p < A.n_passes; ++p) {
                 const int4 pinfo = s_pass[p];
-                for (int gi = pinfo.x; gi < pinfo.y; ++gi, ++seq) {
+                for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
+                    if (s_goff[gi] >= 0) continue;
                     mbar_wait_p(&b_full[seq % UM_SLOTS], (seq / UM_SLOTS) & 1, pa, 2, pon);
                     if (elect_one()) mbar_arrive_leader_relaxed(&b_full[seq % UM_SLOTS]);
                     __syncwarp();
+                    ++seq;
                 }
             }
         }
@@ -652,6 +671,16 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         // The fp32 window of a tile is a contiguous sample range of the clip; one elected
         // converter thread bulk-copies it into the staging buffer one unit ahead.
         const int ct = threadIdx.x - 64;  // 0 .. UM_CONV_THREADS-1
+        // window wb of unit wcnt is converted (all converter threads passed bar 1): tell the
+        // MMA issuer -- the leader's own barrier, directly from the peer CTA too
+        auto window_ready = [&](uint32_t wb, uint32_t wcnt) {
+            if (CG == 2 && !leader) {
+                if (A.dbg & 8) mbar_arrive_leader(&win_full[wb]);  // diagnostics: cluster-scope release
+                else mbar_arrive_leader_cta(&win_full[wb]);
+            } else {
+                mbar_arrive(&win_full[wb]);
+            }
+        };
         const int cw = warp - 2;
         const int chunks = A.win_rows * A.panels * 8;  // 8-sample chunks in the window
         const int64_t wlen = (int64_t)A.win_rows * A.V;
@@ -729,6 +758,23 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     ex = 14 - ex;
                 }
                 const float sc = ldexpf(1.0f, ex);
+                // split into hi/lo fp16 in registers (in place: 8 fp32 -> 4 hi + 4 lo words)
+                // while the window buffer is still busy; only the stores wait for it
+#pragma unroll
+                for (int i = 0; i < CONV_RC; ++i) {
+                    uint32_t w[8];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 a = make_float2(v[i][2 * k] * sc, v[i][2 * k + 1] * sc);
+                        const __half2 h = __float22half2_rn(a);
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __float22half2_rn(make_float2(a.x - hf.x, a.y - hf.y));
+                        w[k] = *reinterpret_cast<const uint32_t *>(&h);
+                        w[4 + k] = *reinterpret_cast<const uint32_t *>(&l);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) v[i][k] = __uint_as_float(w[k]);
+                }
                 if (ct == 0) WH_TRACE(5, wcnt);
                 mbar_wait_p(&win_empty[wb], ((wcnt / A.win_bufs) & 1) ^ 1, pa, 1, pon);
                 if (ct == 0) WH_TRACE(6, wcnt);
@@ -740,27 +786,23 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     if (c < chunks) {
                         const int row = c >> cpr_shift, cc = c & cpr_mask;
                         const int panel = cc >> 3, c8 = cc & 7;
-                        uint32_t hw[4], lw[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 a = make_float2(v[i][2 * k] * sc, v[i][2 * k + 1] * sc);
-                            const __half2 h = __float22half2_rn(a);
-                            const float2 hf = __half22float2(h);
-                            const __half2 l = __float22half2_rn(make_float2(a.x - hf.x, a.y - hf.y));
-                            hw[k] = *reinterpret_cast<const uint32_t *>(&h);
-                            lw[k] = *reinterpret_cast<const uint32_t *>(&l);
-                        }
                         const uint32_t off = (uint32_t)panel * panel_bytes + (uint32_t)row * 128u +
                                              (uint32_t)((c8 ^ (row & 7)) * 16);
-                        *reinterpret_cast<uint4 *>(whi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                        *reinterpret_cast<uint4 *>(wlo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                        *reinterpret_cast<uint4 *>(whi + off) =
+                            make_uint4(__float_as_uint(v[i][0]), __float_as_uint(v[i][1]), __float_as_uint(v[i][2]),
+                                       __float_as_uint(v[i][3]));
+                        *reinterpret_cast<uint4 *>(wlo + off) =
+                            make_uint4(__float_as_uint(v[i][4]), __float_as_uint(v[i][5]), __float_as_uint(v[i][6]),
+                                       __float_as_uint(v[i][7]));
                     }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (ct == 0) xring[wcnt & 3] = ldexpf(1.0f, -ex);
                 asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
-                if (ct == 0) WH_TRACE(7, wcnt);
-                if (lane == 0) mbar_arrive(&win_full[wb]);
+                if (ct == 0) {
+                    WH_TRACE(7, wcnt);
+                    window_ready(wb, wcnt);
+                }
             }
         } else {
         if (A.use_stg && ct == 0 && u0 < n_units) issue(u0);
@@ -858,8 +900,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
             // staging is free again: prefetch the next item's window
             if (A.use_stg && ct == 0 && item + ustride < n_units) issue(item + ustride);
-            if (ct == 0) WH_TRACE(7, wcnt);
-            if (lane == 0) mbar_arrive(&win_full[wb]);
+            if (ct == 0) {
+                WH_TRACE(7, wcnt);
+                window_ready(wb, wcnt);
+            }
         }
         }
     } else {
@@ -1098,7 +1142,7 @@ static int ncheck_tiles(const Plan &p) {
     for (auto &t : p.tiles)
         if ((int64_t)t.k * 64 / p.V >= 4096 || p.V / 64 > 16 || t.c0 > 255 || t.ncols > 255 || (t.byte_off & 127))
             return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table out of range");
-    if (16 * p.passes.size() + 16 * p.groups_u.size() + 8 * p.tiles.size() + 4 * (size_t)p.S > 32 * 1024)
+    if (16 * p.passes.size() + 20 * p.groups_u.size() + 16 * p.tiles.size() + 4 * (size_t)p.S > 32 * 1024)
         return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table too large");
     return WH_OK;
 }
@@ -1200,21 +1244,56 @@ int umma_prepare(Plan &p) {
     WH_CUDA_TRY(cudaFuncGetAttributes(&fa0, kern0));
     const int64_t tables_est = 16 * (int64_t)p.passes.size() + 24 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S;
     const int64_t budget0 = (int64_t)optin0 - (int64_t)fa0.sharedSizeBytes - 1024 - 64 - tables_est;
-    // Resident tap bank: when this CTA's share of the whole bank fits beside one window it
-    // is loaded once per kernel and never streamed (no per-K-step barriers at all).
-    p.resident = (bank_cta + win <= budget0 && std::getenv("WH_UMMA_NO_RESIDENT") == nullptr) ? 1 : 0;
-    int64_t group_target = p.resident ? 48 * 1024 : ((int64_t)p.tiles.size() >= 64 ? 48 * 1024 : 24 * 1024);
-    if (const char *g = std::getenv("WH_UMMA_GROUP_KB")) group_target = std::max(1, std::atoi(g)) * 1024;
+    // Tap residency.  (1) the whole bank fits beside two windows: load it once, never
+    // stream.  (2) it fits beside one window only: "hybrid" -- keep the prefix of the tiles
+    // (in consumption order) resident, stream the tail K-steps of every unit through a small
+    // ring, and spend the freed smem on a second window so window conversion overlaps the
+    // MMAs (opt-in, WH_UMMA_HYBRID: on c2 the per-group waits of the streamed tail cost more
+    // than the hidden conversion; default is one window, all resident).  (3) otherwise
+    // stream everything.
+    const int64_t n_tiles = (int64_t)p.tiles.size();
+    const bool allow_res = std::getenv("WH_UMMA_NO_RESIDENT") == nullptr;
+    int64_t t_split = 0;  // tiles [0, t_split) resident
+    int hybrid = 0;
+    int64_t stream_target = 0;
+    if (allow_res && bank_cta + 2 * win <= budget0) {
+        t_split = n_tiles;
+    } else if (allow_res && bank_cta + win <= budget0) {
+        t_split = n_tiles;
+        if (std::getenv("WH_UMMA_HYBRID") != nullptr) {
+            stream_target = 8 * 1024;
+            int64_t hyb_ring = 32 * 1024;
+            if (const char *r = std::getenv("WH_UMMA_HYB_RING_KB")) hyb_ring = std::max(8, std::atoi(r)) * 1024;
+            const int64_t res_limit = budget0 - 2 * win - hyb_ring;
+            int64_t acc = 0, t = 0;
+            while (t < n_tiles && acc + tile_unit * p.tiles[t].ncols <= res_limit) acc += tile_unit * p.tiles[t++].ncols;
+            int64_t max_tail_tile = 0;
+            for (int64_t i = t; i < n_tiles; ++i) max_tail_tile = std::max(max_tail_tile, tile_unit * p.tiles[i].ncols);
+            if (t > 0 && t < n_tiles && 2 * max_tail_tile <= hyb_ring) {
+                t_split = t;
+                hybrid = 1;
+            }
+        }
+    }
+    p.resident = t_split > 0 ? 1 : 0;
+    const int64_t group_target = p.resident ? 48 * 1024 : (n_tiles >= 64 ? 48 * 1024 : 24 * 1024);
+    int64_t group_target_env = 0;
+    if (const char *g = std::getenv("WH_UMMA_GROUP_KB")) group_target_env = std::max(1, std::atoi(g)) * 1024;
     p.groups_u.clear();
-    int64_t max_group = 0;
+    int64_t max_group = 0, res_bytes = 0;
+    int n_stream = 0;
     for (auto &ps : p.passes) {
         ps.group_begin = (int32_t)p.groups_u.size();
         int t = ps.tile_begin;
         while (t < ps.tile_end) {
+            const bool res = t < t_split;  // groups never straddle the split
+            const int64_t target =
+                group_target_env ? group_target_env : (res ? group_target : (hybrid ? stream_target : group_target));
             UmmaGroup gr{};
             gr.tile_begin = t;
             int64_t bytes = 0;
-            while (t < ps.tile_end && (bytes == 0 || bytes + tile_unit * p.tiles[t].ncols <= group_target)) {
+            while (t < ps.tile_end && (t < t_split) == res &&
+                   (bytes == 0 || bytes + tile_unit * p.tiles[t].ncols <= target)) {
                 p.tiles[t].in_off = (int32_t)bytes;
                 bytes += tile_unit * p.tiles[t].ncols;
                 ++t;
@@ -1222,20 +1301,28 @@ int umma_prepare(Plan &p) {
             gr.tile_end = t;
             gr.cta_bytes = (int32_t)bytes;
             gr.bank_off = byte_off;
+            gr.pad_ = res ? (int32_t)res_bytes : -1;  // smem offset of a resident group
+            if (res) {
+                res_bytes += bytes;
+            } else {
+                ++n_stream;
+                max_group = std::max(max_group, bytes);
+            }
             for (int i = gr.tile_begin; i < gr.tile_end; ++i) {
                 p.tiles[i].byte_off = byte_off + p.tiles[i].in_off;
                 p.tiles[i].blk1_delta = bytes;
             }
             byte_off += bytes * p.cg;
-            max_group = std::max(max_group, bytes);
             p.groups_u.push_back(gr);
         }
         ps.group_end = (int32_t)p.groups_u.size();
     }
     p.bank_bytes = byte_off;
-    const int64_t stage_bytes = max_group;
+    p.res_bytes = res_bytes;
+    p.n_stream = n_stream;
+    const int64_t stage_bytes = std::max<int64_t>(max_group, 1024);
     const int64_t table_bytes = 16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
-                                8 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S;
+                                16 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S;
     // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
     // alignment slack and the tables
     UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
@@ -1247,14 +1334,13 @@ int umma_prepare(Plan &p) {
     const int64_t budget = (int64_t)optin - (int64_t)fa.sharedSizeBytes - 1024 - 64 - table_bytes;
     if (ncheck_tiles(p) != WH_OK) return WH_E_UNSUPPORTED;
     // smem = window buffers (hi|lo fp16) [+ fp32 staging, same bytes as one window] + the
-    // tap-tile ring.  Long units (many K-steps per window) favour a deeper ring with one
-    // window; short units favour double-buffered windows.
-    const int64_t tiles_per_unit = (int64_t)p.tiles.size();
+    // tap stage region (resident groups, then the ring).  Long units (many K-steps per
+    // window) favour a deeper ring with one window; short units favour two windows.
     int use_stg = 0;
     int64_t ring = 0;
-    if (p.resident) {
-        // the "ring" is the whole resident bank; spend what is left on windows / staging
-        ring = (bank_cta + 1023) / 1024 * 1024;
+    if (p.resident && !hybrid) {
+        // the stage region is the whole resident bank; spend what is left on windows / staging
+        ring = (res_bytes + 1023) / 1024 * 1024;
         const int opts_r[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
         for (auto &o : opts_r)
             if ((int64_t)(o[0] + o[1]) * win + ring <= budget) {
@@ -1262,10 +1348,15 @@ int umma_prepare(Plan &p) {
                 use_stg = o[1];
                 break;
             }
-        if (win_bufs == 0) p.resident = 0, ring = 0;
-    }
-    if (!p.resident) {
-        const int prefer_single = tiles_per_unit >= 64 && std::getenv("WH_UMMA_PREFER_DOUBLE") == nullptr;
+        if (win_bufs == 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: resident bank does not fit");
+    } else if (hybrid) {
+        const int64_t rest = (budget - 2 * win - res_bytes) / 1024 * 1024;
+        if (rest < 2 * stage_bytes) return fail(WH_E_UNSUPPORTED, "UMMA engine: hybrid ring does not fit");
+        win_bufs = 2;
+        use_stg = 0;
+        ring = res_bytes + rest;
+    } else {
+        const int prefer_single = n_tiles >= 64 && std::getenv("WH_UMMA_PREFER_DOUBLE") == nullptr;
         const int opts_a[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
         const int opts_b[4][2] = {{1, 1}, {2, 1}, {1, 0}, {2, 0}};
         const int (*opts)[2] = prefer_single ? opts_b : opts_a;
@@ -1287,14 +1378,6 @@ int umma_prepare(Plan &p) {
         }
     }
     if (ring == 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: shared memory too small for the tap ring");
-    // smem offset of every group inside the ring when the bank is resident
-    {
-        int64_t off = 0;
-        for (auto &g : p.groups_u) {
-            g.pad_ = (int32_t)off;
-            off += g.cta_bytes;
-        }
-    }
     bstages = (int)(ring / stage_bytes);
     p.win_bufs = win_bufs;
     p.bstages = bstages;
@@ -1339,6 +1422,8 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.win_bufs = p.win_bufs; a.n_acc = p.n_acc; a.acc_stride = p.acc_stride;
     a.use_stg = p.use_stg;
     a.resident = p.resident;
+    a.res_bytes = (uint32_t)p.res_bytes;
+    a.n_stream = p.n_stream;
     a.cpr_shift = p.panels == 1 ? 3 : p.panels == 2 ? 4 : p.panels == 4 ? 5 : -1;
     a.conv_regs = (!p.use_stg && (int64_t)p.win_rows * p.panels * 8 <= 10 * 128 && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
