@@ -47,6 +47,7 @@ struct UmmaTile {                  // one K-step (64 taps) of one pass
     int32_t k;                     // K-step index (g in [64k, 64k+64))
     int32_t c0;                    // first active column (multiple of 16)
     int32_t ncols;                 // cols - c0
+    int32_t ncorr;                 // cols - c1: columns whose split-fp16 cross terms are kept
     int32_t in_off;                // byte offset of the tile inside its group's CTA block
     int64_t byte_off;              // bank offset of the tile (CTA-0 block of its group)
     int64_t blk1_delta;            // cg = 2: bytes from the CTA-0 block to the CTA-1 block

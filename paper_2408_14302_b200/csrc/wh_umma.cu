@@ -233,6 +233,7 @@ __device__ __forceinline__ void umma_commit(uint64_t *b) {
                      : "memory");
 }
 
+__device__ __forceinline__ int lane_id() { return (int)(threadIdx.x & 31); }
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile("{\n.reg .pred P1;\nelect.sync _|P1, 0xffffffff;\nselp.b32 %0, 1, 0, P1;\n}\n" : "=r"(pred));
@@ -279,6 +280,21 @@ __device__ __forceinline__ float out_value(float mag) {
     else return mag;
 }
 
+// Output stores bypass L1 allocation: the scalogram is written once and never re-read by
+// this kernel, and plain L1-allocating stores were measured to slow the concurrent UMMA
+// operand reads (shared memory and L1 share the SM's data SRAM).
+__device__ __forceinline__ void st_na(float *p, float v) {
+    asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_na(float2 *p, float2 v) {
+    asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_na(float4 *p, float4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+
 // Store R consecutive frames (nvalid of them valid) of one scale row starting at element o.
 template <int R, int CC, int OUT>
 __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nvalid, const float (&re)[R],
@@ -288,11 +304,11 @@ __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nval
         if (R % 2 == 0 && nvalid == R && vec) {
 #pragma unroll
             for (int r = 0; r < R; r += 2)
-                *reinterpret_cast<float4 *>(dst + r) = make_float4(re[r], im[r], re[(r + 1) % R], im[(r + 1) % R]);
+                st_na(reinterpret_cast<float4 *>(dst + r), make_float4(re[r], im[r], re[(r + 1) % R], im[(r + 1) % R]));
         } else {
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (r < nvalid) dst[r] = make_float2(re[r], im[r]);
+                if (r < nvalid) st_na(dst + r, make_float2(re[r], im[r]));
         }
     } else {
         float val[R];
@@ -313,14 +329,14 @@ __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nval
         if (R % 4 == 0 && nvalid == R && vec) {
 #pragma unroll
             for (int r = 0; r < R; r += 4)
-                *reinterpret_cast<float4 *>(dst + r) =
-                    make_float4(val[r], val[(r + 1) % R], val[(r + 2) % R], val[(r + 3) % R]);
+                st_na(reinterpret_cast<float4 *>(dst + r),
+                      make_float4(val[r], val[(r + 1) % R], val[(r + 2) % R], val[(r + 3) % R]));
         } else if (R == 2 && nvalid == 2 && vec) {
-            *reinterpret_cast<float2 *>(dst) = make_float2(val[0], val[1 % R]);
+            st_na(reinterpret_cast<float2 *>(dst), make_float2(val[0], val[1 % R]));
         } else {
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (r < nvalid) dst[r] = val[r];
+                if (r < nvalid) st_na(dst + r, val[r]);
         }
     }
 }
@@ -343,8 +359,101 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
             const int sl0 = u0 / CP;
             float v[16], wr[16];
             tmem_ld16x2(tbase + u0, cbase - u0, v, wr);
-            tmem_st16_zero(tbase + u0);
-            tmem_st16_zero(cbase - u0);
+            if (!(A.dbg & 64)) {  // diagnostics: 64 = skip the re-zeroing (results invalid)
+                tmem_st16_zero(tbase + u0);
+                tmem_st16_zero(cbase - u0);
+            }
+            if (A.dbg & 32) continue;  // diagnostics: 32 = skip the stores
+            if constexpr ((P == 1 || P == 2) && OUT != WH_OUT_COMPLEX64) {
+                // P = 1: one frame per lane -- transpose 4x4 blocks inside each lane quad (two
+                // xor-shuffle stages); P = 2: two frames per lane -- swap halves inside each
+                // lane pair.  Either way every lane then stores 4 consecutive frames of one
+                // scale with one 16-byte store: a quarter (half) of the store requests of
+                // per-lane scalar (8-byte) stores, which compete with the UMMA operand reads
+                // for the SM's data path.
+                const int li = lane_id();
+                float val[SPU][P];
+#pragma unroll
+                for (int q = 0; q < SPU; ++q) {
+                    const float f = (sl0 + q < ns) ? e * spow[s0 + sl0 + q] : 0.0f;
+#pragma unroll
+                    for (int r = 0; r < P; ++r) {
+                        const float x = (v[q * CP + r] + wr[15 - (q * CP + r)]) * f;
+                        float mag;
+                        if constexpr (CC == 2) {
+                            const float y = (v[q * CP + P + r] + wr[15 - (q * CP + P + r)]) * f;
+                            mag = sqrtf(fmaf(x, x, y * y));
+                        } else {
+                            mag = fabsf(x);
+                        }
+                        val[q][r] = out_value<OUT>(mag);
+                    }
+                }
+                if (A.minmax) {
+#pragma unroll
+                    for (int q = 0; q < SPU; ++q)
+#pragma unroll
+                        for (int r = 0; r < P; ++r)
+                            if (sl0 + q < ns && r < nvalid) {
+                                lmin = fminf(lmin, val[q][r]);
+                                lmax = fmaxf(lmax, val[q][r]);
+                            }
+                }
+                constexpr int LPG = 4 / P;  // lanes per 4-frame group (4 or 2)
+                const int gi = li & (LPG - 1);
+                const int64_t fq = frame0 - (int64_t)gi * P;  // first frame of the lane group
+                const int nq = (int)(F - fq < 4 ? (F - fq > 0 ? F - fq : 0) : 4);
+#pragma unroll
+                for (int g = 0; g < SPU / LPG; ++g) {
+                    float t[4];
+                    if constexpr (P == 1) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) t[k] = val[4 * g + k][0];
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {  // exchange the off-diagonal 2x2 blocks
+                            const float s = (gi & 2) ? t[k] : t[2 + k];
+                            const float x = __shfl_xor_sync(0xffffffffu, s, 2);
+                            if (gi & 2) t[k] = x;
+                            else t[2 + k] = x;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; k += 2) {  // transpose the 2x2 blocks
+                            const float s = (gi & 1) ? t[k] : t[k + 1];
+                            const float x = __shfl_xor_sync(0xffffffffu, s, 1);
+                            if (gi & 1) t[k] = x;
+                            else t[k + 1] = x;
+                        }
+                    } else {
+                        // even lane keeps scale 2g (frames fq, fq+1 own, fq+2, fq+3 from the
+                        // odd lane), odd lane keeps scale 2g+1
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const float s = gi ? val[2 * g][k] : val[2 * g + 1][k];
+                            const float x = __shfl_xor_sync(0xffffffffu, s, 1);
+                            if (gi) {
+                                t[k] = x;
+                                t[2 + k] = val[2 * g + 1][k];
+                            } else {
+                                t[k] = val[2 * g][k];
+                                t[2 + k] = x;
+                            }
+                        }
+                    }
+                    // this lane now holds scale sl0 + LPG*g + gi for frames fq .. fq + 3
+                    const int sc = sl0 + LPG * g + gi;
+                    if (sc < ns && nq > 0) {
+                        float *dst = reinterpret_cast<float *>(A.out) + (b * A.S + s0 + sc) * F + fq;
+                        if (nq == 4 && vec) {
+                            st_na(reinterpret_cast<float4 *>(dst), make_float4(t[0], t[1], t[2], t[3]));
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                if (j < nq) st_na(dst + j, t[j]);
+                        }
+                    }
+                }
+                continue;
+            }
             if (nvalid <= 0) continue;
             float re[SPU][P], im[SPU][P];
 #pragma unroll
@@ -456,12 +565,12 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)A.V, panel = (kg % (uint32_t)A.V) >> 6;
         // pre-decoded MMA operands of the K-step, in 16-byte descriptor units:
         //   x = A offset in the window | c0 << 16,   y = B offset in the group | B2 delta << 16,
-        //   z = instruction descriptor of MMA1 (N = 2nc), w = of MMA2 (N = nc)
+        //   z = instruction descriptor of MMA1 (N = nc + ncorr), w = of MMA2 (N = ncorr; 0 = none)
         const uint32_t aoff = panel * (uint32_t)A.win_rows * 128u + q * 128u;
-        const uint32_t nc = (uint32_t)tl.ncols;
-        const uint32_t b2d = (CG == 2 ? nc : 2 * nc) * 128u;
+        const uint32_t n1 = (uint32_t)(tl.ncols + tl.ncorr), n2 = (uint32_t)tl.ncorr;
+        const uint32_t b2d = (CG == 2 ? n1 / 2 : n1) * 128u;
         s_tile[i] = make_uint4((aoff >> 4) | ((uint32_t)tl.c0 << 16), ((uint32_t)tl.in_off >> 4) | ((b2d >> 4) << 16),
-                               idesc_f16<CG>(2 * nc), idesc_f16<CG>(nc));
+                               idesc_f16<CG>(n1), n2 ? idesc_f16<CG>(n2) : 0u);
     }
 
     if (threadIdx.x == 0) {
@@ -614,8 +723,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     }
                     const uint32_t g16 = gbase >> 4;
                     for (int t = gr.x; t < gr.y; ++t) {
-                        // MMA1: A_hi x [hi_c0..hi_C-1 | lo_C-1..lo_c0] -> main_j at col j, corr_j at 2C-1-j
-                        // MMA2: A_lo x [hi_C-1..hi_c0]               -> corr
+                        // MMA1: A_hi x [hi_c0..hi_C-1 | lo_C-1..lo_c1] -> main_j at col j, corr_j at 2C-1-j
+                        // MMA2: A_lo x [hi_C-1..hi_c1]               -> corr   (skipped if c1 = C)
                         // (CG = 2: each CTA's stage holds half of every B operand).  Descriptor
                         // low words are 16-byte smem addresses (< 2^14): no masking needed.
                         const uint4 tt = s_tile[t];
@@ -623,10 +732,16 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
                         const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
                         if (!(A.dbg & 4) && elect_one()) {
+                            if (tt.w) {
 #pragma unroll
-                            for (uint32_t j = 0; j < 4; ++j) {
-                                umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
-                                umma_f16<CG>(d2, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
+                                for (uint32_t j = 0; j < 4; ++j) {
+                                    umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                                    umma_f16<CG>(d2, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
+                                }
+                            } else {
+#pragma unroll
+                                for (uint32_t j = 0; j < 4; ++j)
+                                    umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
                             }
                         }
                         __syncwarp();
@@ -1033,11 +1148,11 @@ __global__ void k_build_bank(BankArgs a) {
     const UmmaTile tl = a.tiles[t];
     const int CP = a.Cc * a.P;
     const int C = ps.cols;
-    // cg = 1: [hi fwd | lo rev | hi rev] (nc rows each, one CTA holds the whole tile)
-    // cg = 2: block of CTA 0 = [hi fwd | hi rev rows 0..nc/2), block of CTA 1 =
-    //         [lo rev | hi rev rows nc/2..nc) -- each CTA holds half of every MMA's B
+    // MMA1's B = [hi fwd (nc rows, columns c0..C-1) | lo rev (ncorr rows, C-1..c1)],
+    // MMA2's B = hi rev (ncorr rows).  cg = 1: the tile is [MMA1 B | MMA2 B];  cg = 2: each
+    // CTA's block is [its half of MMA1 B | its half of MMA2 B] (CTA 0 the first halves)
     uint8_t *tile0 = a.bank + tl.byte_off;
-    const int nc = tl.ncols;
+    const int nc = tl.ncols, ncorr = tl.ncorr, n1 = nc + ncorr;
     const double norm = pow(M_PI * a.Bw, -0.5);
     const double w = 2.0 * M_PI * a.C;
     for (int idx = threadIdx.x; idx < tl.ncols * 64; idx += blockDim.x) {
@@ -1073,16 +1188,25 @@ __global__ void k_build_bank(BankArgs a) {
             *reinterpret_cast<__half *>(base + off) = val;
         };
         const int rrev = C - 1 - col;  // row index in the reversed parts
+        const bool corr = rrev < ncorr;
         if (a.cg == 2) {
             uint8_t *blk0 = tile0, *blk1 = tile0 + tl.blk1_delta;
-            put(blk0, n, h);
-            put(blk1, rrev, l);
-            if (rrev < nc / 2) put(blk0, nc + rrev, h);
-            else put(blk1, nc + rrev - nc / 2, h);
+            auto put1 = [&](int row, __half val) {  // row of MMA1's B
+                if (row < n1 / 2) put(blk0, row, val);
+                else put(blk1, row - n1 / 2, val);
+            };
+            put1(n, h);
+            if (corr) {
+                put1(nc + rrev, l);
+                if (rrev < ncorr / 2) put(blk0, n1 / 2 + rrev, h);
+                else put(blk1, n1 / 2 + rrev - ncorr / 2, h);
+            }
         } else {
             put(tile0, n, h);
-            put(tile0 + (size_t)nc * 128, rrev, l);
-            put(tile0 + (size_t)nc * 256, rrev, h);
+            if (corr) {
+                put(tile0, nc + rrev, l);
+                put(tile0 + (size_t)n1 * 128, rrev, h);
+            }
         }
     }
 }
@@ -1179,6 +1303,8 @@ int umma_prepare(Plan &p) {
     }
 
     const int CP = p.Cc * p.P;
+    int tau_log2 = 12;  // correction-term threshold tau = 2^-12 (WH_UMMA_TAU=0: never skip)
+    if (const char *t = std::getenv("WH_UMMA_TAU")) tau_log2 = std::atoi(t);
     // TMEM: 512 columns = 2 accumulator buffers x (128 main + 128 correction) columns, so a
     // pass covers at most 128 columns and the epilogue of pass n overlaps the MMAs of n+1.
     const int max_cols = 128;
@@ -1216,11 +1342,30 @@ int umma_prepare(Plan &p) {
                 }
             }
             if (c0 >= ps.ns * CP) continue;  // no active column on this K-step
+            // correction columns: the split-fp16 cross terms x_h*t_l + x_l*t_h matter only
+            // where a column's taps are not negligible: with every |tap| of the K-step below
+            // tau * (the scale's peak tap) the dropped terms are < 2^-10 * tau of |x|*|t|
+            // summed over a Gaussian tail (mass fraction < 1e-4): far below the fp32
+            // accumulation error.  Bound |tap| by the envelope exp(-u^2 / (B a^2)).
+            int c1 = ps.cols;
+            for (int j = c0; j < ps.ns * CP; ++j) {
+                const int s = ps.s0 + j / CP, r = j % p.P;
+                const int64_t u0 = (int64_t)k * 64 - p.G0 - (int64_t)r * H, u1 = u0 + 63;
+                const int64_t umin = (u0 <= 0 && u1 >= 0) ? 0 : std::min(std::llabs(u0), std::llabs(u1));
+                if ((double)umin > (double)p.half[s]) continue;  // inactive column
+                const double x = (double)umin / p.scales[s];
+                if (tau_log2 <= 0 || -(x * x) / p.B > -tau_log2 * M_LN2) {
+                    c1 = j;
+                    break;
+                }
+            }
             c0 = c0 / 16 * 16;
+            c1 = c1 / 16 * 16;
             UmmaTile tl{};
             tl.k = k;
             tl.c0 = c0;
             tl.ncols = ps.cols - c0;
+            tl.ncorr = ps.cols - c1;
             max_tile_cols = std::max(max_tile_cols, tl.ncols);
             p.tiles.push_back(tl);
         }
@@ -1232,9 +1377,13 @@ int umma_prepare(Plan &p) {
     // Group consecutive tiles of a pass into one bulk copy of up to group_target bytes per
     // CTA: a copy costs ~250 issue cycles whatever its size (tools/probe_bulk.cu), so small
     // tiles must travel together.  Bank layout per group: [CTA-0 blocks][CTA-1 blocks].
-    const int64_t tile_unit = p.cg == 2 ? 192 : 384;  // bytes per column per CTA
+    // bytes per CTA of a tile: MMA1's B has nc + ncorr rows, MMA2's ncorr (128 B per row);
+    // CTA pairs hold half of each
+    auto tile_bytes = [&](const UmmaTile &t) -> int64_t {
+        return (int64_t)(p.cg == 2 ? 64 : 128) * (t.ncols + 2 * t.ncorr);
+    };
     int64_t bank_cta = 0;
-    for (auto &t : p.tiles) bank_cta += tile_unit * t.ncols;
+    for (auto &t : p.tiles) bank_cta += tile_bytes(t);
     // budget known early: the opt-in smem minus static smem and slack (tables added below)
     UmmaKernel kern0 = umma_kernel(p.Cc, p.P, p.cg);
     if (!kern0) return fail(WH_E_UNSUPPORTED, "UMMA engine: unsupported phase count");
@@ -1266,9 +1415,9 @@ int umma_prepare(Plan &p) {
             if (const char *r = std::getenv("WH_UMMA_HYB_RING_KB")) hyb_ring = std::max(8, std::atoi(r)) * 1024;
             const int64_t res_limit = budget0 - 2 * win - hyb_ring;
             int64_t acc = 0, t = 0;
-            while (t < n_tiles && acc + tile_unit * p.tiles[t].ncols <= res_limit) acc += tile_unit * p.tiles[t++].ncols;
+            while (t < n_tiles && acc + tile_bytes(p.tiles[t]) <= res_limit) acc += tile_bytes(p.tiles[t++]);
             int64_t max_tail_tile = 0;
-            for (int64_t i = t; i < n_tiles; ++i) max_tail_tile = std::max(max_tail_tile, tile_unit * p.tiles[i].ncols);
+            for (int64_t i = t; i < n_tiles; ++i) max_tail_tile = std::max(max_tail_tile, tile_bytes(p.tiles[i]));
             if (t > 0 && t < n_tiles && 2 * max_tail_tile <= hyb_ring) {
                 t_split = t;
                 hybrid = 1;
@@ -1293,9 +1442,9 @@ int umma_prepare(Plan &p) {
             gr.tile_begin = t;
             int64_t bytes = 0;
             while (t < ps.tile_end && (t < t_split) == res &&
-                   (bytes == 0 || bytes + tile_unit * p.tiles[t].ncols <= target)) {
+                   (bytes == 0 || bytes + tile_bytes(p.tiles[t]) <= target)) {
                 p.tiles[t].in_off = (int32_t)bytes;
-                bytes += tile_unit * p.tiles[t].ncols;
+                bytes += tile_bytes(p.tiles[t]);
                 ++t;
             }
             gr.tile_end = t;
@@ -1341,13 +1490,21 @@ int umma_prepare(Plan &p) {
     if (p.resident && !hybrid) {
         // the stage region is the whole resident bank; spend what is left on windows / staging
         ring = (res_bytes + 1023) / 1024 * 1024;
-        const int opts_r[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
-        for (auto &o : opts_r)
+        // the register-prefetch converter (no fp32 staging) is the faster one when a
+        // thread's share of the window fits its registers
+        const bool regs_ok = (int64_t)p.win_rows * p.panels * 8 <= 10 * 128;
+        const int opts_stg[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
+        const int opts_regs[4][2] = {{2, 0}, {1, 0}, {2, 1}, {1, 1}};
+        const int (*opts_r)[2] = regs_ok ? opts_regs : opts_stg;
+        const int r0 = std::getenv("WH_UMMA_WIN1") ? (regs_ok ? 1 : 2) : 0;  // diagnostics: one window
+        for (int i = r0; i < 4; ++i) {
+            const int *o = opts_r[i];
             if ((int64_t)(o[0] + o[1]) * win + ring <= budget) {
                 win_bufs = o[0];
                 use_stg = o[1];
                 break;
             }
+        }
         if (win_bufs == 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: resident bank does not fit");
     } else if (hybrid) {
         const int64_t rest = (budget - 2 * win - res_bytes) / 1024 * 1024;

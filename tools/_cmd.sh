@@ -1,4 +1,3 @@
 timeout 400 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
-for e in "" "WH_UMMA_DBG=8"; do echo "== $e"; env $e timeout 60 python tools/trace_units.py --config c2 2>&1 | sed -n 1,5p | cut -c1-200
-env $e timeout 120 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], '%.3e coeffs/s' % d['value'], '%.4f ms' % d['ms_per_step'], d['clocks']['sm_mhz'])"; done
-for c in c5 c4h16 c3 c1; do timeout 120 python bench.py --config $c --clips $([ $c = c5 ] && echo 296 || echo 0) --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], '%.3e coeffs/s' % d['value'], '%.4f ms' % d['ms_per_step'], d['clocks']['sm_mhz'])"; done
+for c in c2 c5 c3 c4h16 c4h64 c1; do timeout 120 python bench.py --config $c --clips $([ $c = c5 ] && echo 296 || echo 0) --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], '%.3e coeffs/s' % d['value'], '%.4f ms' % d['ms_per_step'], d['clocks']['sm_mhz'])"; done
+timeout 60 python tools/gpu_check.py umma 2>&1 | tail -14
