@@ -480,14 +480,14 @@ int wh_plan_trace(wh_plan *plan, int32_t enable, int64_t *events, int32_t n) {
     cudaGetDevice(&prev);
     WH_CUDA_TRY(cudaSetDevice(p->device));
     if (!p->d_trace) {
-        WH_CUDA_TRY(cudaMalloc(&p->d_trace, sizeof(long long) * 16 * 32));
-        WH_CUDA_TRY(cudaMemset(p->d_trace, 0, sizeof(long long) * 16 * 32));
+        WH_CUDA_TRY(cudaMalloc(&p->d_trace, sizeof(long long) * WH_TRACE_N));
+        WH_CUDA_TRY(cudaMemset(p->d_trace, 0, sizeof(long long) * WH_TRACE_N));
     }
     if (events && n > 0) {
-        long long h[16 * 32];
+        static long long h[WH_TRACE_N];
         WH_CUDA_TRY(cudaDeviceSynchronize());
         WH_CUDA_TRY(cudaMemcpy(h, p->d_trace, sizeof h, cudaMemcpyDeviceToHost));
-        for (int i = 0; i < n && i < 16 * 32; ++i) events[i] = h[i];
+        for (int i = 0; i < n && i < WH_TRACE_N; ++i) events[i] = h[i];
     }
     if (!enable) {
         cudaFree(p->d_trace);

@@ -11,6 +11,10 @@
 
 namespace wh {
 
+// diagnostics trace buffer (wh_plan_trace): CTA-0 timeline [16 events][32 units] of clock64,
+// then per CTA (up to 256) the %globaltimer (ns) at kernel entry and exit
+constexpr int WH_TRACE_N = 16 * 32 + 2 * 256;
+
 // Thread-local last-error message behind wh_last_error().
 void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
@@ -62,6 +66,7 @@ struct UmmaGroup {                 // consecutive tiles of a pass fetched by one
 struct Plan {
     int device = 0;
     int sms = 148;
+    int grid_ctas = 148;                   // UMMA: co-resident CTAs (pairs x 2) of the persistent grid
     int32_t S = 0;
     std::vector<double> scales;
     std::vector<int64_t> half;     // L_s (fp64 ceil, wavelet.py:154)

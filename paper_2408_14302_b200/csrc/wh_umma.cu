@@ -3,30 +3,37 @@
 //
 // Math (restating wavelet.py:215-273 / _kernels.py:28-62's polyphase identity):
 //   the signal of one clip is viewed as rows of V samples (V = 64 when hop | 64, else
-//   V = hop for hop % 64 == 0).  A frame at sample position m*V + r*hop (row m, phase
-//   r = 0..P-1, P = V/hop) correlates with taps over offsets u in [-L, L]:
-//       W(s, m*P + r) = sum_g X[m - Qlo + floor(g/V), g mod V] * B[g, (s, r)]
-//   with B[g, (s, c, r)] = tap_{s,c}(g - Qlo*V - r*hop)  (c = re / im component).
-//   X's rows for K-step k are X rows shifted by floor(64k/V): the whole window of a
-//   128-row tile is converted ONCE into shared memory (fp32 -> hi/lo fp16, 128B
-//   swizzle) and every K-step's A operand is the same buffer with its UMMA descriptor
-//   start moved by q*128 B (tools/probe_umma_shift.cu verified the absolute-address
-//   swizzle makes this exact).  The taps B are a constant bank, pre-swizzled in HBM
-//   (L2-resident), streamed per K-step with cp.async.bulk.
-//   Precision: x*2^e = xh + xl, t*2^f = th + tl (fp16 each); D += xh*th + xh*tl + xl*th
-//   in fp32 (the dropped xl*tl term is ~2^-22 relative), then D * 2^-(e+f).
+//   V = hop for hop % 64 == 0).  Frame (row m, phase r = 0..P-1, P = V/hop) sits at sample
+//   m*V + r*hop and correlates with taps over offsets u in [-L, L].  With the K index
+//   g = u + G0 (G0 = Lmax rounded up to 4):
+//       W(s, m*P + r) = sum_g x[m*V - G0 + g] * B[g, (s, c, r)],
+//       B[g, (s, c, r)] = tap_{s,c}(g - G0 - r*hop)        (c = re / im component)
+//   and x[m*V - G0 + g] = X[m + floor(g/V), g mod V] for the window X of rows of V samples
+//   starting at sample tile*128*V - G0.  K-step k's A operand is that window shifted by
+//   floor(64k/V) rows: the window of a 128-row tile is converted ONCE into shared memory
+//   (fp32 -> hi/lo fp16, 128 B swizzle) and every K-step's UMMA descriptor start moves by
+//   q*128 B (tools/probe_umma_shift.cu verified the absolute-address swizzle makes this
+//   exact).  The taps B are a constant bank, pre-swizzled on the device at plan time:
+//   resident in shared memory when it fits, else streamed per tap group with cp.async.bulk.
+//   Precision: x*2^e = xh + xl, t*2^f = th + tl (fp16 each); main += xh*th and, in a
+//   separate accumulator, corr += xh*tl + xl*th (fp32, TMEM); the cross terms are skipped
+//   on tap tails below 2^-12 of the scale's peak; W = (main + corr) * 2^-(e+f).
 //
-// CTA roles (256 threads, 1 CTA per SM, persistent over (clip, row-tile) items):
-//   warp 0      producer: cp.async.bulk of tap tiles into a byte ring of variable-size slots
-//   warp 1      TMEM allocator + MMA issuer (one elected thread)
-//   warps 2-3   converters: window max -> exponent -> hi/lo fp16 swizzled window
-//   warps 4-7   epilogue: tcgen05.ld -> scale, |W| / log1p / ... -> global stores,
-//               per-clip min/max atomics
+// CTA roles (448 threads, 1 CTA per SM, CTA pairs (cta_group::2, M = 256), persistent over
+// units = (clip, pair of 128-row tiles)):
+//   warp 0      producer: cp.async.bulk of the resident bank / streamed tap groups
+//   warp 1      leader CTA: TMEM allocator + MMA issuer (one elected thread);
+//               peer CTA: relays "tap group landed" to the leader's barriers
+//   warps 2-5   converters: window -> registers -> max -> exponent -> hi/lo fp16, stored
+//               swizzled once the window buffer is free
+//   warps 6-13  epilogue (2 per TMEM lane quadrant): tcgen05.ld main + corr -> scale,
+//               |W| / power / log_db / log1p -> 16-byte global stores, per-clip min/max
 #include <cuda_fp16.h>
 #include <math.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -46,7 +53,7 @@ struct UmmaArgs {
     int64_t ld_x, N, F, hop;
     int64_t items;              // clips * row_tiles
     int64_t clips;
-    int32_t row_tiles, V, P, Cc, panels, Qlo, win_rows, S;
+    int32_t row_tiles, V, P, Cc, panels, G0, win_rows, S;
     int32_t n_passes, n_tiles, wavelet, output, win_bufs, vec_ok;
     int32_t n_acc, acc_stride;          // accumulator buffers; columns per buffer (main|corr)
     int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
@@ -233,6 +240,11 @@ __device__ __forceinline__ void umma_commit(uint64_t *b) {
                      : "memory");
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ int lane_id() { return (int)(threadIdx.x & 31); }
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
@@ -526,6 +538,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
+        A.trace[16 * 32 + 2 * blockIdx.x] = (long long)globaltimer_ns();
+        if (blockIdx.x == 0) A.trace[14 * 32] = clock64();  // SM clock rate = cycles / ns
+    }
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // 0 = leader (issues the MMAs)
     const bool leader = rank == 0;
     // work units: (clip, CG consecutive 128-row tiles); CTA `rank` of a pair takes tile
@@ -804,7 +820,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         auto staged = [&](int64_t item, int64_t &lo, int64_t &hi) {
             int64_t b, tile;
             unit_tile(item, b, tile);
-            const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
+            const int64_t w0 = tile * 128 * A.V - A.G0;
             lo = w0 > 0 ? w0 : 0;
             hi = w0 + wlen < A.N ? w0 + wlen : (A.N & ~(int64_t)3);
             if (!A.vec_ok || !A.use_stg || hi <= lo) { lo = hi = w0; }
@@ -815,7 +831,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             staged(item, lo, hi);
             int64_t b, tile;
             unit_tile(item, b, tile);
-            const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
+            const int64_t w0 = tile * 128 * A.V - A.G0;
             const uint32_t bytes = (uint32_t)((hi - lo) * 4);
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
@@ -830,7 +846,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
                 int64_t b, tile;
                 unit_tile(item, b, tile);
-                const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
+                const int64_t w0 = tile * 128 * A.V - A.G0;
                 const float *xb = A.x + b * A.ld_x;
                 const uint32_t wb = wcnt % A.win_bufs;
                 const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);
@@ -925,7 +941,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
             int64_t b, tile;
             unit_tile(item, b, tile);
-            const int64_t w0 = (tile * 128 - A.Qlo) * A.V;
+            const int64_t w0 = tile * 128 * A.V - A.G0;
             const float *xb = A.x + b * A.ld_x;
             const uint32_t wb = wcnt % A.win_bufs;
             int64_t slo, shi;
@@ -1113,6 +1129,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     }
     tc_fence_before();
     cta_pair_sync<CG>();
+    if (A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
+        A.trace[16 * 32 + 2 * blockIdx.x + 1] = (long long)globaltimer_ns();
+        if (blockIdx.x == 0) A.trace[14 * 32 + 1] = clock64();
+    }
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();
@@ -1241,9 +1261,8 @@ int umma_supported(const Plan &p, std::string *why) {
         return WH_E_UNSUPPORTED;
     }
     const int64_t V = small ? 64 : H;
-    const int64_t Qlo = (p.Lmax + V - 1) / V;
     const int64_t P = V / H;
-    const int64_t maxg = Qlo * V + p.Lmax + (P - 1) * H;
+    const int64_t maxg = (p.Lmax + V - 1) / V * V + p.Lmax + (P - 1) * H;  // longest K range of the planner
     const int64_t ksteps = maxg / 64 + 1;
     const int64_t qmax = (ksteps - 1) * 64 / V;
     const int64_t rows = ((128 + qmax) + 7) / 8 * 8;
@@ -1281,15 +1300,8 @@ int umma_prepare(Plan &p) {
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
     p.panels = p.V / 64;
-    p.Qlo = (int32_t)((p.Lmax + p.V - 1) / p.V);
-    p.G0 = p.Qlo * p.V;
-    const int64_t maxg = (int64_t)p.G0 + p.Lmax + (int64_t)(p.P - 1) * H;
-    p.ksteps = (int32_t)(maxg / 64 + 1);
-    const int64_t qmax = (int64_t)(p.ksteps - 1) * 64 / p.V;
-    p.win_rows = (int32_t)(((128 + qmax) + 7) / 8 * 8);
     p.rows_total = (int32_t)((p.F + p.P - 1) / p.P);
     p.row_tiles = (p.rows_total + 127) / 128;
-    const int64_t win = 2LL * p.panels * p.win_rows * 128;
 
     // per-scale exponent: max|tap| = (pi B)^-1/2 / sqrt(a) scaled into [2^13, 2^14)
     p.fexp.resize(p.S);
@@ -1314,64 +1326,97 @@ int umma_prepare(Plan &p) {
     // scales per pass: whole scales, cols = ns*CP rounded up to 16 (CP > 256 unsupported)
     if (CP > max_cols) return fail(WH_E_UNSUPPORTED, "UMMA engine: too many phases per scale");
     const int spp = std::max(1, max_cols / CP);
-    p.passes.clear();
-    p.tiles.clear();
-    int64_t byte_off = 0;
-    int max_tile_cols = 16;
-    // heavy (long-tap) passes first so the accumulator pipeline starts on the long ones
-    std::vector<std::pair<int, int>> ranges;
-    for (int s0 = 0; s0 < p.S; s0 += spp) ranges.push_back({s0, std::min(spp, p.S - s0)});
-    std::reverse(ranges.begin(), ranges.end());
-    for (auto &rg : ranges) {
-        UmmaPass ps{};
-        ps.s0 = rg.first;
-        ps.ns = rg.second;
-        ps.cols = (ps.ns * CP + 15) / 16 * 16;
-        ps.tile_begin = (int32_t)p.tiles.size();
-        // column activity: column j = (scale, comp, phase) active on g in
-        // [G0 - L + r*H, G0 + L + r*H]
-        for (int k = 0; k < p.ksteps; ++k) {
-            int c0 = ps.cols;
-            for (int j = 0; j < ps.ns * CP; ++j) {
-                const int s = ps.s0 + j / CP, r = j % p.P;
-                const int64_t lo = p.G0 - p.half[s] + (int64_t)r * H;
-                const int64_t hi = p.G0 + p.half[s] + (int64_t)r * H;
-                if (hi >= (int64_t)k * 64 && lo <= (int64_t)k * 64 + 63) {
-                    c0 = j;
-                    break;
+    // Passes and K-step tiles for a K origin G0 (K index g = u + G0, tap offset u in
+    // [-L, L]); returns the modelled MMA cycles per unit (tools/probe_kstep.cu: a K-step
+    // costs max(its shared-memory operand reads, its tensor work) + issue overhead).
+    auto make_tiles = [&](int64_t G0, std::vector<UmmaPass> &passes, std::vector<UmmaTile> &tiles) -> double {
+        passes.clear();
+        tiles.clear();
+        const int64_t ksteps = (G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1;
+        double cost = 0.0;
+        // heavy (long-tap) passes first so the accumulator pipeline starts on the long ones
+        for (int s0 = ((p.S - 1) / spp) * spp; s0 >= 0; s0 -= spp) {
+            UmmaPass ps{};
+            ps.s0 = s0;
+            ps.ns = std::min(spp, p.S - s0);
+            ps.cols = (ps.ns * CP + 15) / 16 * 16;
+            ps.tile_begin = (int32_t)tiles.size();
+            for (int64_t k = 0; k < ksteps; ++k) {
+                // first active column: column j = (scale, comp, phase) is active on g in
+                // [G0 - L + r*H, G0 + L + r*H]
+                int c0 = ps.cols;
+                for (int j = 0; j < ps.ns * CP; ++j) {
+                    const int s = ps.s0 + j / CP, r = j % p.P;
+                    const int64_t lo = G0 - p.half[s] + (int64_t)r * H;
+                    const int64_t hi = G0 + p.half[s] + (int64_t)r * H;
+                    if (hi >= k * 64 && lo <= k * 64 + 63) {
+                        c0 = j;
+                        break;
+                    }
                 }
-            }
-            if (c0 >= ps.ns * CP) continue;  // no active column on this K-step
-            // correction columns: the split-fp16 cross terms x_h*t_l + x_l*t_h matter only
-            // where a column's taps are not negligible: with every |tap| of the K-step below
-            // tau * (the scale's peak tap) the dropped terms are < 2^-10 * tau of |x|*|t|
-            // summed over a Gaussian tail (mass fraction < 1e-4): far below the fp32
-            // accumulation error.  Bound |tap| by the envelope exp(-u^2 / (B a^2)).
-            int c1 = ps.cols;
-            for (int j = c0; j < ps.ns * CP; ++j) {
-                const int s = ps.s0 + j / CP, r = j % p.P;
-                const int64_t u0 = (int64_t)k * 64 - p.G0 - (int64_t)r * H, u1 = u0 + 63;
-                const int64_t umin = (u0 <= 0 && u1 >= 0) ? 0 : std::min(std::llabs(u0), std::llabs(u1));
-                if ((double)umin > (double)p.half[s]) continue;  // inactive column
-                const double x = (double)umin / p.scales[s];
-                if (tau_log2 <= 0 || -(x * x) / p.B > -tau_log2 * M_LN2) {
-                    c1 = j;
-                    break;
+                if (c0 >= ps.ns * CP) continue;  // no active column on this K-step
+                // correction columns: the split-fp16 cross terms x_h*t_l + x_l*t_h matter only
+                // where a column's taps are not negligible: with every |tap| of the K-step
+                // below tau * (the scale's peak tap) the dropped terms are < 2^-10 * tau of
+                // |x|*|t| summed over a Gaussian tail (mass fraction < 1e-4): far below the
+                // fp32 accumulation error.  |tap| is bounded by the envelope exp(-u^2/(B a^2)).
+                int c1 = ps.cols;
+                for (int j = c0; j < ps.ns * CP; ++j) {
+                    const int s = ps.s0 + j / CP, r = j % p.P;
+                    const int64_t u0 = k * 64 - G0 - (int64_t)r * H, u1 = u0 + 63;
+                    const int64_t umin = (u0 <= 0 && u1 >= 0) ? 0 : std::min(std::llabs(u0), std::llabs(u1));
+                    if ((double)umin > (double)p.half[s]) continue;  // inactive column
+                    const double x = (double)umin / p.scales[s];
+                    if (tau_log2 <= 0 || -(x * x) / p.B > -tau_log2 * M_LN2) {
+                        c1 = j;
+                        break;
+                    }
                 }
+                UmmaTile tl{};
+                tl.k = (int32_t)k;
+                tl.c0 = c0 / 16 * 16;
+                tl.ncols = ps.cols - tl.c0;
+                tl.ncorr = ps.cols - c1 / 16 * 16;
+                tiles.push_back(tl);
+                const double rows = tl.ncols + 2.0 * tl.ncorr;
+                cost += std::max(128.0 * (tl.ncorr ? 2 : 1) + 0.5 * rows + 50.0, 2.0 * rows + 30.0);
             }
-            c0 = c0 / 16 * 16;
-            c1 = c1 / 16 * 16;
-            UmmaTile tl{};
-            tl.k = k;
-            tl.c0 = c0;
-            tl.ncols = ps.cols - c0;
-            tl.ncorr = ps.cols - c1;
-            max_tile_cols = std::max(max_tile_cols, tl.ncols);
-            p.tiles.push_back(tl);
+            ps.tile_end = (int32_t)tiles.size();
+            if (ps.tile_end > ps.tile_begin) passes.push_back(ps);
         }
-        ps.tile_end = (int32_t)p.tiles.size();
-        if (ps.tile_end > ps.tile_begin) p.passes.push_back(ps);
+        return cost;
+    };
+    // K origin: G0 >= Lmax, a multiple of 32 samples (the window start tile*128*V - G0 on a
+    // 128-byte line: whole sectors for the converters' loads).  Candidates up to one row
+    // later are modelled; whole-row alignment (G0 % V == 0) wins unless it models > 3 %
+    // slower (measured: hop 256 runs 6 % faster row-aligned at equal tiles; c2 runs 3 %
+    // faster with 21 instead of 22 K-steps), then the smaller G0.
+    {
+        std::vector<UmmaPass> tp;
+        std::vector<UmmaTile> tt;
+        const int64_t g0min = (p.Lmax + 31) / 32 * 32;
+        int64_t best = -1;
+        double best_cost = 0.0;
+        for (int64_t g0 = g0min; g0 <= g0min + p.V; g0 += 32) {
+            const double c = make_tiles(g0, tp, tt) * (g0 % p.V == 0 ? 1.0 : 1.03);
+            if (best < 0 || c < best_cost - 0.5) {
+                best = g0;
+                best_cost = c;
+            }
+        }
+        if (const char *g = std::getenv("WH_UMMA_G0_ALIGN")) {  // diagnostics: force an alignment
+            const int64_t al = std::max(4, std::atoi(g)) / 4 * 4;
+            best = (p.Lmax + al - 1) / al * al;
+        }
+        p.G0 = (int32_t)best;
     }
+    make_tiles(p.G0, p.passes, p.tiles);
+    p.Qlo = (int32_t)((p.G0 + p.V - 1) / p.V);
+    p.ksteps = (int32_t)((p.G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1);
+    const int64_t qmax = (int64_t)(p.ksteps - 1) * 64 / p.V;
+    p.win_rows = (int32_t)(((128 + qmax) + 7) / 8 * 8);
+    const int64_t win = 2LL * p.panels * p.win_rows * 128;
+    int64_t byte_off = 0;
     // CTA pairs (tcgen05 cta_group::2, M = 256): each CTA stages half of every tap tile
     p.cg = (p.sms % 2 == 0 && std::getenv("WH_UMMA_CG1") == nullptr) ? 2 : 1;
     // Group consecutive tiles of a pass into one bulk copy of up to group_target bytes per
@@ -1565,6 +1610,39 @@ int umma_prepare(Plan &p) {
     WH_CUDA_TRY(cudaDeviceSynchronize());
     cudaFree(d_fexp);
     WH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
+    // persistent grid: as many CTAs (pairs) as can be co-resident -- with clusters of 2 not
+    // every SM necessarily has a partner in its GPC, and a CTA pair that does not fit would
+    // run its whole unit sequence as a second wave
+    p.grid_ctas = p.sms;
+    if (p.cg == 2) {
+        WH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)p.sms);
+        cfg.blockDim = dim3(UM_THREADS);
+        cfg.dynamicSmemBytes = p.smem_bytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) == cudaSuccess && clusters > 0)
+            p.grid_ctas = std::min(p.sms, 2 * clusters);
+        (void)cudaGetLastError();
+    }
+    if (std::getenv("WH_UMMA_VERBOSE")) {  // diagnostics: the plan's shape
+        int64_t ncorr = 0, ncols = 0;
+        for (auto &t : p.tiles) ncols += t.ncols, ncorr += t.ncorr;
+        std::fprintf(stderr,
+                     "[wh umma] V=%d P=%d Cc=%d cg=%d passes=%zu tiles=%zu (sum nc %lld, ncorr %lld) groups=%zu "
+                     "resident=%d res=%lld B stream_groups=%d bank/CTA=%lld B win=%d x %lld B stg=%d ring=%lld B "
+                     "smem=%zu B grid=%d CTAs\n",
+                     p.V, p.P, p.Cc, p.cg, p.passes.size(), p.tiles.size(), (long long)ncols, (long long)ncorr,
+                     p.groups_u.size(), p.resident, (long long)p.res_bytes, p.n_stream, (long long)bank_cta,
+                     p.win_bufs, (long long)win, p.use_stg, (long long)p.ring_bytes, p.smem_bytes, p.grid_ctas);
+    }
     return WH_OK;
 }
 
@@ -1573,7 +1651,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.x = x; a.ld_x = ld_x; a.N = p.N; a.F = p.F; a.hop = p.hop;
     a.items = clips * p.row_tiles;
     a.row_tiles = p.row_tiles; a.V = p.V; a.P = p.P; a.Cc = p.Cc; a.panels = p.panels;
-    a.Qlo = p.Qlo; a.win_rows = p.win_rows; a.S = p.S;
+    a.G0 = p.G0; a.win_rows = p.win_rows; a.S = p.S;
     a.n_passes = (int32_t)p.passes.size(); a.n_tiles = (int32_t)p.tiles.size();
     a.wavelet = p.wavelet; a.output = p.output;
     a.win_bufs = p.win_bufs; a.n_acc = p.n_acc; a.acc_stride = p.acc_stride;
@@ -1598,7 +1676,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.dbg = std::getenv("WH_UMMA_DBG") ? std::atoi(std::getenv("WH_UMMA_DBG")) : 0;
     a.trace = p.d_trace;
     const int64_t units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
-    int64_t grid = std::min<int64_t>(units * p.cg, p.sms);
+    int64_t grid = std::min<int64_t>(units * p.cg, p.grid_ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     cudaLaunchConfig_t cfg = {};

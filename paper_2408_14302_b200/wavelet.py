@@ -212,11 +212,15 @@ class CwthPlan:
         roles = ("producer", "mma", "converter", "epilogue", "relay")
         return {r: list(buf[i * 4:(i + 1) * 4]) for i, r in enumerate(roles)}
 
-    def trace(self, enable: bool = True):
-        """Diagnostics: CTA-0 timeline of the UMMA kernel, int64 [16 events, 32 units]."""
-        buf = (ctypes.c_int64 * (16 * 32))()
-        _lib.check(_lib.load().wh_plan_trace(self._h, int(enable), buf, 16 * 32))
-        return np.array(buf, dtype=np.int64).reshape(16, 32)
+    def trace(self, enable: bool = True, per_cta: bool = False):
+        """Diagnostics: CTA-0 timeline of the UMMA kernel, int64 [16 events, 32 units] of
+        clock64; with ``per_cta`` also int64 [256, 2] %globaltimer ns at CTA entry / exit."""
+        n = 16 * 32 + 2 * 256
+        buf = (ctypes.c_int64 * n)()
+        _lib.check(_lib.load().wh_plan_trace(self._h, int(enable), buf, n))
+        a = np.array(buf, dtype=np.int64)
+        t = a[:512].reshape(16, 32)
+        return (t, a[512:].reshape(256, 2)) if per_cta else t
 
     # -- execution ------------------------------------------------------------------
     def _check_input(self, clips: int, n: int):

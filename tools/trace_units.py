@@ -32,3 +32,20 @@ for u in range(12):
     if t[1, u] == 0:
         break
     print(f"{u:4d} " + " ".join(f"{(t[e, u] - t0) / 1e3:13.1f}" for e in range(len(names))))
+
+# per-CTA entry/exit (globaltimer ns) of the traced launch
+plan.trace(True)
+t0ev = torch.cuda.Event(enable_timing=True)
+t1ev = torch.cuda.Event(enable_timing=True)
+t0ev.record()
+plan.execute(x, out)
+t1ev.record()
+torch.cuda.synchronize()
+tt, c = plan.trace(False, per_cta=True)
+cyc = tt[14, 1] - tt[14, 0]
+ns = c[0, 1] - c[0, 0]
+print(f"CTA 0: {cyc} cycles in {ns} ns -> {cyc / ns * 1e3:.0f} MHz")
+c = c[(c[:, 0] > 0)]
+base = c[:, 0].min()
+print(f"launch (events) {t0ev.elapsed_time(t1ev) * 1e3:.1f} us; CTAs {len(c)}: entry spread {(c[:, 0].max() - base) / 1e3:.1f} us, "
+      f"exit min {(c[:, 1].min() - base) / 1e3:.1f} us median {(np.median(c[:, 1]) - base) / 1e3:.1f} us max {(c[:, 1].max() - base) / 1e3:.1f} us")
