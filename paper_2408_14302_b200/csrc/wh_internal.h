@@ -94,6 +94,7 @@ struct Plan {
 
     // UMMA engine
     int32_t V = 64, P = 1, Cc = 1, panels = 1;
+    int32_t rs = 1;                        // UMMA rows per frame (hop = 256 * rs > 256)
     int32_t Qlo = 0, G0 = 0, ksteps = 0, win_rows = 0;  // window rows (multiple of 8)
     int32_t rows_total = 0, row_tiles = 0;
     std::vector<UmmaPass> passes;

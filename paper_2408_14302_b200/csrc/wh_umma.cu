@@ -54,6 +54,7 @@ struct UmmaArgs {
     int64_t items;              // clips * row_tiles
     int64_t clips;
     int32_t row_tiles, V, P, Cc, panels, G0, win_rows, S;
+    int32_t rs;                         // rows per frame (hop = 256 * rs > 256), else 1
     int32_t n_passes, n_tiles, wavelet, output, win_bufs, vec_ok;
     int32_t n_acc, acc_stride;          // accumulator buffers; columns per buffer (main|corr)
     int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
@@ -376,7 +377,7 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                 tmem_st16_zero(cbase - u0);
             }
             if (A.dbg & 32) continue;  // diagnostics: 32 = skip the stores
-            if constexpr ((P == 1 || P == 2) && OUT != WH_OUT_COMPLEX64) {
+            if constexpr ((P == 1 || P == 2) && OUT != WH_OUT_COMPLEX64) if (A.rs == 1) {
                 // P = 1: one frame per lane -- transpose 4x4 blocks inside each lane quad (two
                 // xor-shuffle stages); P = 2: two frames per lane -- swap halves inside each
                 // lane pair.  Either way every lane then stores 4 consecutive frames of one
@@ -1050,8 +1051,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             int64_t b, tile;
             unit_tile(item, b, tile);
             const int64_t mrow = tile * 128 + m;  // global row (beyond rows_total: no frames)
-            const int64_t frame0 = mrow * P;      // first frame of this row
-            const int64_t rem_frames = A.F - frame0;
+            // first frame of this row (rs > 1: only every rs-th row is a frame)
+            const int64_t frame0 = A.rs > 1 ? mrow / A.rs : mrow * P;
+            const int64_t rem_frames = (A.rs > 1 && mrow % A.rs) ? 0 : A.F - frame0;
             const int nvalid = rem_frames <= 0 ? 0 : (rem_frames >= P ? P : (int)rem_frames);
             if (A.minmax && b != cur_b) {
                 if (cur_b >= 0) {
@@ -1254,15 +1256,16 @@ static UmmaKernel umma_kernel(int Cc, int P, int CG) {
 
 int umma_supported(const Plan &p, std::string *why) {
     const int64_t H = p.hop;
-    bool small = H <= 64 && 64 % H == 0;
-    bool big = H % 64 == 0 && H <= 256;
-    if (!small && !big) {
-        if (why) *why = "hop must divide 64 or be a multiple of 64 up to 256";
+    const bool small = H <= 64 && 64 % H == 0;
+    const bool big = H % 64 == 0 && H <= 256;
+    const bool strided = H > 256 && H % 256 == 0;  // rows of 256 samples, every (H/256)-th a frame
+    if (!small && !big && !strided) {
+        if (why) *why = "hop must divide 64, or be a multiple of 64 up to 256, or a multiple of 256";
         return WH_E_UNSUPPORTED;
     }
-    const int64_t V = small ? 64 : H;
-    const int64_t P = V / H;
-    const int64_t maxg = (p.Lmax + V - 1) / V * V + p.Lmax + (P - 1) * H;  // longest K range of the planner
+    const int64_t V = small ? 64 : (big ? H : 256);
+    const int64_t P = strided ? 1 : V / H;
+    const int64_t maxg = (p.Lmax + V - 1) / V * V + p.Lmax + (P - 1) * (strided ? 0 : H);  // longest K range
     const int64_t ksteps = maxg / 64 + 1;
     const int64_t qmax = (ksteps - 1) * 64 / V;
     const int64_t rows = ((128 + qmax) + 7) / 8 * 8;
@@ -1291,16 +1294,25 @@ static int ncheck_tiles(const Plan &p) {
 }
 
 int umma_prepare(Plan &p) {
-    const int64_t H = p.hop;
+    // hop | 64: rows of 64 samples, P = 64/hop frames (phases) per row; hop = 64..256 (multiple
+    // of 64): one frame per row of hop samples; hop = 256*RS: rows of 256 samples of which
+    // every RS-th is a frame (the other rows are computed and dropped: RS x the tensor work,
+    // still far ahead of the SIMT engine)
+    int64_t H = p.hop;
+    p.rs = 1;
+    if (H > 256) {
+        p.rs = (int32_t)(H / 256);
+        H = 256;
+    }
     p.V = (int32_t)(H <= 64 ? 64 : H);
     if (const char *vm = std::getenv("WH_UMMA_VMUL")) {  // diagnostics: rows of V * vmul samples
         const int vmul = std::atoi(vm);
-        if (vmul == 2 || vmul == 4) p.V = std::min<int32_t>(p.V * vmul, 256);
+        if ((vmul == 2 || vmul == 4) && p.rs == 1) p.V = std::min<int32_t>(p.V * vmul, 256);
     }
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
     p.panels = p.V / 64;
-    p.rows_total = (int32_t)((p.F + p.P - 1) / p.P);
+    p.rows_total = (int32_t)(p.rs > 1 ? (p.F - 1) * p.rs + 1 : (p.F + p.P - 1) / p.P);
     p.row_tiles = (p.rows_total + 127) / 128;
 
     // per-scale exponent: max|tap| = (pi B)^-1/2 / sqrt(a) scaled into [2^13, 2^14)
@@ -1650,7 +1662,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     UmmaArgs a{};
     a.x = x; a.ld_x = ld_x; a.N = p.N; a.F = p.F; a.hop = p.hop;
     a.items = clips * p.row_tiles;
-    a.row_tiles = p.row_tiles; a.V = p.V; a.P = p.P; a.Cc = p.Cc; a.panels = p.panels;
+    a.row_tiles = p.row_tiles; a.V = p.V; a.P = p.P; a.Cc = p.Cc; a.panels = p.panels; a.rs = p.rs;
     a.G0 = p.G0; a.win_rows = p.win_rows; a.S = p.S;
     a.n_passes = (int32_t)p.passes.size(); a.n_tiles = (int32_t)p.tiles.size();
     a.wavelet = p.wavelet; a.output = p.output;

@@ -29,7 +29,7 @@ ENGINES = ("umma", "simt")
 
 
 def umma_ok(hop):
-    return (hop <= 64 and 64 % hop == 0) or (hop % 64 == 0 and hop <= 256)
+    return (hop <= 64 and 64 % hop == 0) or (hop % 64 == 0 and hop <= 256) or hop % 256 == 0
 
 
 def engines_for(hop):
@@ -254,7 +254,9 @@ def test_ragged_and_tiny_signals(engine):
 
 def test_engine_selection_and_errors():
     assert wh.CwthPlan([1.0, 2.0], None, 64, 1000).engine == "umma"
+    assert wh.CwthPlan([1.0, 2.0], None, 1024, 5000).engine == "umma"  # rows of 256, every 4th a frame
     assert wh.CwthPlan([1.0, 2.0], None, 7, 1000).engine == "simt"
+    assert wh.CwthPlan([1.0, 2.0], None, 320, 5000).engine == "simt"
     with pytest.raises(wh.DeviceError):
         wh.CwthPlan([1.0, 2.0], None, 7, 1000, engine="umma")
     with pytest.raises(wh.InvalidHop):
