@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define WH_ABI_VERSION 1
+#define WH_ABI_VERSION 2
 
 /* Error codes.  The Python host maps them onto the reference exception types of
  * errors.py: WH_E_INVALID_HOP -> InvalidHop (errors.py:24, raised by
@@ -64,8 +64,12 @@ enum {
 };
 
 /* Per-clip normalisation of real outputs: MINMAX maps each clip's (S, F) map
- * affinely onto [0, 1], constant clip -> 0 (scalogram.py:77-83 without x255). */
-enum { WH_NORM_NONE = 0, WH_NORM_MINMAX = 1 };
+ * affinely onto [0, 1], constant clip -> 0 (scalogram.py:77-83 without x255).
+ * RENDER_U8 is render(magnitude(...)) of scalogram.py:67-86 per clip: uint8
+ * [clips][S][F], floor((v - lo) * 255 / (hi - lo) + 0.5) in float64, constant clip -> 0,
+ * rows flipped (image row 0 = the last scale, flip_vertical=True); _NOFLIP keeps the
+ * scale order (flip_vertical=False). */
+enum { WH_NORM_NONE = 0, WH_NORM_MINMAX = 1, WH_NORM_RENDER_U8 = 2, WH_NORM_RENDER_U8_NOFLIP = 3 };
 
 /* Compute engine.  AUTO picks the tcgen05 split-fp16 engine when the hop allows a
  * polyphase tiling, else the SIMT fp32 engine.  There is no CPU engine. */
@@ -134,6 +138,22 @@ int wh_strided_correlate(int device, const double *xpad, int64_t xpad_len, const
 int wh_strided_correlate_symmetric(int device, const double *xpad, int64_t xpad_len,
                                    const double *re_half, const double *im_half, int64_t half,
                                    int64_t hop, int64_t frames, double *out_re, double *out_im);
+
+/* Data formats either side of the path.
+ *
+ * signal_io.py:130-150 decimate(signal, hop, anti_alias) on device buffers: out[b][i] =
+ * x[b][i*hop] for i < ceil(n_samples/hop); with anti_alias the reference's low-pass
+ * (scipy firwin(10*hop+1, 0.9/hop): Hamming window, unit DC gain) is applied first as a
+ * "same"-centred linear convolution, accumulated in float64.  This is the front half of
+ * cwth_decimate (wavelet.py:276-294); the back half is a hop-1 plan on the output.
+ * Errors: WH_E_INVALID_HOP, WH_E_EMPTY_SIGNAL, WH_E_INVALID_ARG.  Stream-ordered. */
+int wh_decimate(int device, const float *x_dev, int64_t clips, int64_t n_samples, int64_t ld_x,
+                int64_t hop, int32_t anti_alias, float *out_dev, int64_t ld_out, void *stream);
+
+/* scalogram.py:67-86 render(values, flip_vertical) for `count` real matrices of rows x cols
+ * (device float32 [count][rows][cols] -> device uint8, same shape).  Stream-ordered. */
+int wh_render_u8(int device, const float *values_dev, int64_t count, int64_t rows, int64_t cols,
+                 int32_t flip_vertical, uint8_t *out_dev, void *stream);
 
 #ifdef __cplusplus
 }

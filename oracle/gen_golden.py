@@ -11,7 +11,11 @@ seeded inputs, what the reference's own public API returns:
                     half widths L (wavelet.py:154) of every scale in every BASELINE config;
 * ``cwth.npz``   -- cwth_strided (wavelet.py:215-273) complex128 outputs for small
                     versions of c1-c5 plus ragged/edge/impulse/parameter cases, and
-                    magnitude/render (scalogram.py:51-86) outputs.
+                    magnitude/render (scalogram.py:51-86) outputs;
+* ``formats.npz`` -- the SURVEY §8f rows: decimate (signal_io.py:130-150, with and
+                    without the anti-alias FIR), cwth_decimate (wavelet.py:276-294),
+                    render on float32 matrices incl. exact .5 ties and a constant
+                    matrix, and the bytes of write_matrix_bin / write_pgm / write_csv.
 
 The GPU box never reads /root/reference; tests read only these fixtures.
 """
@@ -114,7 +118,57 @@ def main():
     cases["render_abs"] = render(magnitude(m, "abs")).pixels
     cases["render_abs_noflip"] = render(magnitude(m, "abs"), flip_vertical=False).pixels
     np.savez_compressed(os.path.join(OUT, "cwth.npz"), **cases)
-    for f in ("taps.npz", "cwth.npz"):
+
+    # ---- §8f rows: decimate / cwth_decimate / render / file formats -------------------------
+    from wavehop.scalogram import write_csv, write_matrix_bin, write_pgm  # noqa: E402
+    from wavehop.signal_io import decimate  # noqa: E402
+    from wavehop.wavelet import cwth_decimate  # noqa: E402
+    import tempfile  # noqa: E402
+
+    fmt = {}
+    rng = np.random.default_rng(2408_14302_8)
+    for name, n, hop, aa in (("d_n5000_h4", 5000, 4, False), ("d_n5000_h4_aa", 5000, 4, True),
+                             ("d_n4096_h16_aa", 4096, 16, True), ("d_n1001_h7_aa", 1001, 7, True),
+                             ("d_n50_h64_aa", 50, 64, True), ("d_n300_h1_aa", 300, 1, True),
+                             ("d_n300_h1", 300, 1, False)):
+        x = rng.standard_normal(n).astype(np.float32)
+        d = decimate(SignalBuffer(x.astype(np.float64), 16_000.0), hop, aa)
+        fmt[f"{name}__x"] = x
+        fmt[f"{name}__meta"] = np.array([hop, int(aa)], dtype=np.int64)
+        fmt[f"{name}__ref"] = d.samples
+        fmt[f"{name}__rate"] = np.array(d.sample_rate)
+    for name, n, hop, aa, sc in (("cd_h8", 4000, 8, False, np.geomspace(1.0, 12.0, 6)),
+                                 ("cd_h8_aa", 4000, 8, True, np.geomspace(1.0, 12.0, 6)),
+                                 ("cd_h32_aa", 16000, 32, True, np.geomspace(1.5, 20.0, 5))):
+        x = rng.standard_normal(n).astype(np.float32)
+        m = cwth_decimate(SignalBuffer(x.astype(np.float64), 16_000.0), ScaleGrid(sc), params, hop, aa)
+        fmt[f"{name}__x"] = x
+        fmt[f"{name}__scales"] = sc
+        fmt[f"{name}__meta"] = np.array([hop, int(aa), m.hop], dtype=np.int64)
+        fmt[f"{name}__rate"] = np.array(m.source_rate)
+        fmt[f"{name}__ref"] = m.values
+    # render on float32-representable matrices, incl. exact .5 ties and a constant matrix
+    v = rng.standard_normal((7, 33)).astype(np.float32)
+    fmt["render_rand__v"] = v
+    fmt["render_rand__flip"] = render(v.astype(np.float64)).pixels
+    fmt["render_rand__noflip"] = render(v.astype(np.float64), flip_vertical=False).pixels
+    ties = (np.arange(0, 511, dtype=np.float32) / 2.0).reshape(7, 73)  # scaled = k/2 exactly
+    fmt["render_ties__v"] = ties
+    fmt["render_ties__flip"] = render(ties.astype(np.float64)).pixels
+    const = np.full((3, 5), 2.5, dtype=np.float32)
+    fmt["render_const__v"] = const
+    fmt["render_const__flip"] = render(const.astype(np.float64)).pixels
+    # byte-exact writers
+    cm = wavehop.CoefficientMatrix(cases["c5s__ref"], 32, 16_000.0, ScaleGrid(np.geomspace(1, 512, 12)))
+    with tempfile.TemporaryDirectory() as td:
+        write_matrix_bin(cm, os.path.join(td, "m.scg1"))
+        write_pgm(render(magnitude(cm, "abs")), os.path.join(td, "m.pgm"))
+        write_csv(magnitude(cm, "log_db")[:3, :10], os.path.join(td, "m.csv"))
+        for ext in ("scg1", "pgm", "csv"):
+            with open(os.path.join(td, f"m.{ext}"), "rb") as f:
+                fmt[f"file_{ext}"] = np.frombuffer(f.read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "formats.npz"), **fmt)
+    for f in ("taps.npz", "cwth.npz", "formats.npz"):
         print(f, os.path.getsize(os.path.join(OUT, f)), "bytes")
 
 

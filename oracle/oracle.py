@@ -226,3 +226,70 @@ def epilogue(values: np.ndarray, wavelet: str, output: str, norm=None) -> np.nda
         lo, hi = res.min(), res.max()
         res = np.zeros_like(res) if hi == lo else (res - lo) * (1.0 / (hi - lo))
     return res
+
+
+# ---- decimation, render, SCG1 (restated, float64) -------------------
+
+def firwin_lowpass(numtaps: int, cutoff: float) -> np.ndarray:
+    """scipy.signal.firwin(numtaps, cutoff) with its defaults, as the reference calls it
+    (signal_io.py:144; scipy is an unpinned third-party dependency, pkg/pyproject.toml:10-14):
+    the published window method -- ideal low-pass cutoff*sinc(cutoff*(n - (T-1)/2)) times the
+    symmetric Hamming window 0.54 - 0.46*cos(2*pi*n/(T-1)), scaled to unit gain at DC."""
+    n = np.arange(numtaps, dtype=np.float64)
+    m = n - 0.5 * (numtaps - 1)
+    h = cutoff * np.sinc(cutoff * m)
+    if numtaps > 1:
+        h = h * (0.54 - 0.46 * np.cos(2.0 * np.pi * n / (numtaps - 1)))
+    return h / h.sum()
+
+
+def decimate(x: np.ndarray, hop: int, anti_alias: bool = False) -> np.ndarray:
+    """signal_io.py:130-150: [B, N] (or [N]) float64 -> every hop-th sample from index 0;
+    with ``anti_alias`` the FIR firwin(10*hop+1, 0.9/hop) is applied first as a "same"-
+    centred linear convolution (fftconvolve mode="same" keeps full[(T-1)//2 : ... + N])."""
+    x = np.asarray(x, dtype=np.float64)
+    single = x.ndim == 1
+    xx = np.atleast_2d(x)
+    if anti_alias:
+        h = firwin_lowpass(10 * hop + 1, 0.9 / hop)
+        c = (h.size - 1) // 2
+        xx = np.stack([np.convolve(row, h, mode="full")[c:c + row.size] for row in xx])
+    out = xx[:, ::hop].copy()
+    return out[0] if single else out
+
+
+def cwth_decimate_batch(x, scales, hop, anti_alias=False, *, wavelet="cmor", output="complex",
+                        norm=None, center_frequency=1.0, bandwidth=1.5, support_radius=6.0):
+    """wavelet.py:276-294: decimate (above), then the full hop = 1 transform of the
+    decimated signal (direct f64 oracle; the reference's FFT route agrees to ~1e-12)."""
+    d = decimate(np.atleast_2d(np.asarray(x, dtype=np.float64)), hop, anti_alias)
+    if not anti_alias:  # selection keeps float32 samples exact: the C batch oracle applies
+        return cwth_batch(d.astype(np.float32), scales, 1, wavelet=wavelet, output=output,
+                          norm=norm, center_frequency=center_frequency, bandwidth=bandwidth,
+                          support_radius=support_radius)
+    # the filtered signal is not float32-representable: float64 per-clip route
+    vals = np.stack([cwth_strided_routed(row, scales, 1, center_frequency, bandwidth, support_radius)
+                     for row in d])
+    return np.stack([epilogue(v, wavelet, output, norm) for v in vals])
+
+
+def render(values: np.ndarray, flip_vertical: bool = True) -> np.ndarray:
+    """scalogram.py:67-86 -> uint8 pixels: (v - lo) * (255 / (hi - lo)), floor(+0.5), clip;
+    constant -> zeros; flip reverses the rows."""
+    values = np.asarray(values, dtype=np.float64)
+    lo, hi = values.min(), values.max()
+    if hi == lo:
+        px = np.zeros(values.shape, dtype=np.uint8)
+    else:
+        px = np.clip(np.floor((values - lo) * (255.0 / (hi - lo)) + 0.5), 0, 255).astype(np.uint8)
+    return px[::-1] if flip_vertical else px
+
+
+def scg1_bytes(values: np.ndarray, hop: int, source_rate: float, scales: np.ndarray) -> bytes:
+    """scalogram.py:100-106: "SCG1" | <III d (rows, cols, hop, rate) | f64 scales | c8 payload."""
+    import struct
+
+    values = np.asarray(values)
+    rows, cols = values.shape
+    return (b"SCG1" + struct.pack("<III d", rows, cols, hop, source_rate)
+            + np.asarray(scales, dtype="<f8").tobytes() + values.astype("<c8").tobytes())

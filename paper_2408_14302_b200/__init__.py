@@ -8,11 +8,14 @@ CPU fallback.
 """
 
 from .errors import (DeviceError, EmptySignal, InvalidCount, InvalidHop, InvalidRange,
-                     InvalidScale, WavehopError)
-from .scalogram import MAG_MODES, magnitude
-from .signal_io import SignalBuffer
+                     InvalidScale, InvalidSpec, IoFailure, MalformedHeader, MalformedRiff,
+                     TruncatedPayload, UnsupportedEncoding, WavehopError)
+from .scalogram import (MAG_MODES, ScalogramImage, magnitude, read_matrix_bin, render,
+                        render_device, write_csv, write_matrix_bin, write_matrix_bin_raw,
+                        write_pgm)
+from .signal_io import SignalBuffer, decimate, decimate_device
 from .wavelet import (CoefficientMatrix, CwthPlan, MorletParams, ScaleGrid, cwt_fft, cwth_batch,
-                      cwth_strided, get_plan, half_width, make_scale_grid, sample_wavelet,
-                      scale_to_frequency)
+                      cwth_decimate, cwth_decimate_batch, cwth_strided, get_plan, half_width,
+                      make_scale_grid, sample_wavelet, scale_to_frequency)
 
 __version__ = "0.1.0"

@@ -28,7 +28,7 @@ WH_E_OOM = 8
 
 WAVELETS = {"cmor": 0, "rmor": 1}
 OUTPUTS = {"complex": 0, "abs": 1, "power": 2, "log_db": 3, "log1p": 4}
-NORMS = {None: 0, "none": 0, "minmax": 1}
+NORMS = {None: 0, "none": 0, "minmax": 1, "render": 2, "render_noflip": 3}
 ENGINES = {"auto": 0, "simt": 1, "umma": 2}
 ENGINE_NAMES = {v: k for k, v in ENGINES.items()}
 
@@ -56,6 +56,8 @@ SIGNATURES = {
     "wh_strided_correlate": (ctypes.c_int, [ctypes.c_int, _p, _i64, _p, _p, _i64, _i64, _i64, _p, _p]),
     "wh_strided_correlate_symmetric": (ctypes.c_int, [ctypes.c_int, _p, _i64, _p, _p, _i64, _i64, _i64,
                                                       _p, _p]),
+    "wh_decimate": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i64, _i64, _i64, _i32, _p, _i64, _p]),
+    "wh_render_u8": (ctypes.c_int, [ctypes.c_int, _p, _i64, _i64, _i64, _i32, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -31,7 +31,10 @@ int fail(int code, const std::string &msg) {
     return code;
 }
 
-int64_t out_elem_bytes(const Plan &p) { return p.output == WH_OUT_COMPLEX64 ? 8 : 4; }
+int64_t out_elem_bytes(const Plan &p) {
+    if (p.norm == WH_NORM_RENDER_U8 || p.norm == WH_NORM_RENDER_U8_NOFLIP) return 1;
+    return p.output == WH_OUT_COMPLEX64 ? 8 : 4;
+}
 
 // ---------------------------------------------------------------------------------------
 // Filter bank: fp64 sampling of the conjugated, 1/sqrt(a)-normalised Morlet exactly as
@@ -197,7 +200,7 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
     cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
     cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow);
-    cudaFree(p->d_minmax); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
+    cudaFree(p->d_minmax); cudaFree(p->d_scratch); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     cudaSetDevice(cur);
@@ -227,9 +230,9 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
     if (wavelet != WH_WAVELET_CMOR && wavelet != WH_WAVELET_RMOR)
         return fail(WH_E_INVALID_ARG, "unknown wavelet");
     if (output < WH_OUT_COMPLEX64 || output > WH_OUT_LOG1P) return fail(WH_E_INVALID_ARG, "unknown output");
-    if (norm != WH_NORM_NONE && norm != WH_NORM_MINMAX) return fail(WH_E_INVALID_ARG, "unknown norm");
-    if (norm == WH_NORM_MINMAX && output == WH_OUT_COMPLEX64)
-        return fail(WH_E_INVALID_ARG, "min-max normalisation needs a real output");
+    if (norm < WH_NORM_NONE || norm > WH_NORM_RENDER_U8_NOFLIP) return fail(WH_E_INVALID_ARG, "unknown norm");
+    if (norm != WH_NORM_NONE && output == WH_OUT_COMPLEX64)
+        return fail(WH_E_INVALID_ARG, "min-max / render normalisation needs a real output");
     if (engine < WH_ENGINE_AUTO || engine > WH_ENGINE_UMMA) return fail(WH_E_INVALID_ARG, "unknown engine");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -261,9 +264,13 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
     p->max_clips = max_clips; p->output = output; p->norm = norm;
 
     int rc = build_fold_bank(*p);
-    if (rc == WH_OK && norm == WH_NORM_MINMAX) {
+    if (rc == WH_OK && norm != WH_NORM_NONE) {
         if (cudaMalloc(&p->d_minmax, sizeof(uint32_t) * 2 * max_clips) != cudaSuccess)
             rc = fail(WH_E_OOM, "cudaMalloc(minmax) failed");
+    }
+    if (rc == WH_OK && is_render(*p)) {  // float values before the uint8 map
+        if (cudaMalloc(&p->d_scratch, sizeof(float) * (size_t)max_clips * n_scales * p->F) != cudaSuccess)
+            rc = fail(WH_E_OOM, "cudaMalloc(render scratch) failed");
     }
     std::string why;
     if (rc == WH_OK) {
@@ -326,7 +333,7 @@ int wh_plan_out_bytes(const wh_plan *plan, int64_t clips, int64_t *bytes) {
 int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches) {
     if (!plan || !launches) return fail(WH_E_INVALID_ARG, "NULL argument");
     const Plan *p = reinterpret_cast<const Plan *>(plan);
-    *launches = clips > 0 ? (1 + (p->norm == WH_NORM_MINMAX ? 2 : 0)) : 0;
+    *launches = clips > 0 ? (1 + (p->norm != WH_NORM_NONE ? 2 : 0)) : 0;
     return WH_OK;
 }
 
@@ -356,14 +363,21 @@ int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im,
     return WH_OK;
 }
 
+// mm: this call's slice of the per-clip min/max keys; scratch: its slice of the float
+// values a render plan maps to uint8
 static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev, cudaStream_t s,
-                        uint32_t *mm) {
+                        uint32_t *mm, float *scratch) {
     int rc = WH_OK;
-    if (p->norm == WH_NORM_MINMAX) rc = minmax_reset(*p, clips, mm, s);
+    const bool render = is_render(*p);
+    void *dst = render ? static_cast<void *>(scratch) : out_dev;
+    if (p->norm != WH_NORM_NONE) rc = minmax_reset(*p, clips, mm, s);
     if (rc == WH_OK)
-        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, out_dev, s, mm)
-                                           : simt_launch(*p, x_dev, clips, ld_x, out_dev, s, mm);
+        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm)
+                                           : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm);
     if (rc == WH_OK && p->norm == WH_NORM_MINMAX) rc = minmax_apply(*p, clips, out_dev, mm, s);
+    if (rc == WH_OK && render)
+        rc = render_apply(scratch, clips, p->S, p->F, mm, p->norm == WH_NORM_RENDER_U8 ? 1 : 0,
+                          static_cast<uint8_t *>(out_dev), s);
     return rc;
 }
 
@@ -379,7 +393,7 @@ int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, v
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != p->device) WH_CUDA_TRY(cudaSetDevice(p->device));
-    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax);
+    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax, p->d_scratch);
     if (prev != p->device) cudaSetDevice(prev);
     return rc;
 }
@@ -436,7 +450,8 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
             rc = fail(WH_E_CUDA, "H2D copy failed");
             break;
         }
-        rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0);
+        rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0,
+                          p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr);
         if (rc == WH_OK && cudaMemcpyAsync(reinterpret_cast<uint8_t *>(out_host) + (size_t)c0 * out_clip, dout,
                                            (size_t)nc * out_clip, cudaMemcpyDeviceToHost, s) != cudaSuccess)
             rc = fail(WH_E_CUDA, "D2H copy failed");

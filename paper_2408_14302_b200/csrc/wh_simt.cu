@@ -200,7 +200,7 @@ int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     if (clips > 2147483647LL) return fail(WH_E_INVALID_ARG, "too many clips");
     dim3 grid((unsigned)clips, (unsigned)p.n_items);
     bool cplx = p.wavelet == WH_WAVELET_CMOR;
-    if (p.norm != WH_NORM_MINMAX) mm = nullptr;
+    if (p.norm == WH_NORM_NONE) mm = nullptr;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     if (cplx)
         k_simt<true><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,

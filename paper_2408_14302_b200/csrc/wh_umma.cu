@@ -1676,7 +1676,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
-    a.minmax = p.norm == WH_NORM_MINMAX ? mm : nullptr;
+    a.minmax = p.norm != WH_NORM_NONE ? mm : nullptr;
     int max_cols = 16;
     for (auto &t : p.tiles) max_cols = std::max(max_cols, t.ncols);
     a.clips = clips;

@@ -32,3 +32,27 @@ class InvalidRange(WavehopError, ValueError):
 
 class InvalidCount(WavehopError, ValueError):
     """Scale count is not usable for the requested range (errors.py:36)."""
+
+
+class MalformedRiff(WavehopError):
+    """WAV container is structurally broken (errors.py:10)."""
+
+
+class UnsupportedEncoding(WavehopError):
+    """WAV encoding other than 16-bit PCM or 32-bit IEEE float (errors.py:14)."""
+
+
+class InvalidSpec(WavehopError, ValueError):
+    """Synthesis spec violates its constraints (errors.py:28)."""
+
+
+class MalformedHeader(WavehopError):
+    """Coefficient-matrix file header is invalid (errors.py:58)."""
+
+
+class TruncatedPayload(WavehopError):
+    """Coefficient-matrix file ends before the declared payload (errors.py:62)."""
+
+
+class IoFailure(WavehopError):
+    """Reading or writing a file failed (errors.py:66)."""

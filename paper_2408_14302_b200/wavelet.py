@@ -167,7 +167,7 @@ class CwthPlan:
         if output not in _lib.OUTPUTS:
             raise ValueError(f"output must be one of {tuple(_lib.OUTPUTS)}")
         if norm not in _lib.NORMS:
-            raise ValueError("norm must be None or 'minmax'")
+            raise ValueError("norm must be None, 'minmax', 'render' or 'render_noflip'")
         _lib.check(lib.wh_plan_create(
             ctypes.byref(handle), self.device,
             self.scales.ctypes.data_as(ctypes.c_void_p), int(self.scales.size),
@@ -187,6 +187,13 @@ class CwthPlan:
     @property
     def out_shape_per_clip(self):
         return (self.scales.size, self.frames)
+
+    @property
+    def out_dtype(self):
+        """numpy dtype of the output: complex64, float32, or uint8 for render plans."""
+        if self.norm in ("render", "render_noflip"):
+            return np.dtype(np.uint8)
+        return np.dtype(np.complex64 if self.output == "complex" else np.float32)
 
     def launches(self, clips: int) -> int:
         n = ctypes.c_int64()
@@ -235,7 +242,7 @@ class CwthPlan:
         B, n = x.shape
         self._check_input(B, n)
         shape = (B, self.scales.size, self.frames)
-        dtype = np.complex64 if self.output == "complex" else np.float32
+        dtype = self.out_dtype
         if out is None:
             out = np.empty(shape, dtype=dtype)
         elif out.shape != shape or out.dtype != dtype or not out.flags.c_contiguous:
@@ -261,7 +268,8 @@ class CwthPlan:
         B, n = x.shape
         self._check_input(B, n)
         shape = (B, self.scales.size, self.frames)
-        dtype = torch.complex64 if self.output == "complex" else torch.float32
+        dtype = {np.dtype(np.uint8): torch.uint8, np.dtype(np.complex64): torch.complex64,
+                 np.dtype(np.float32): torch.float32}[self.out_dtype]
         if out is None:
             out = torch.empty(shape, dtype=dtype, device=x.device)
         elif tuple(out.shape) != shape or out.dtype != dtype or not out.is_contiguous():
@@ -269,7 +277,8 @@ class CwthPlan:
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        _lib.check(_lib.load().wh_execute(self._h, ctypes.c_void_p(x.data_ptr()), B, x.stride(0),
+        ld_x = x.stride(0) if B > 1 else n  # a size-1 batch dimension may carry stride 0
+        _lib.check(_lib.load().wh_execute(self._h, ctypes.c_void_p(x.data_ptr()), B, ld_x,
                                           ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(handle)))
         return out
 
@@ -367,6 +376,44 @@ def cwth_strided(signal: SignalBuffer, grid: ScaleGrid, params: MorletParams | N
                       wavelet="cmor", output="complex", device=device, engine=engine)[0]
     return CoefficientMatrix(vals.astype(np.complex128), hop, signal.sample_rate,
                              ScaleGrid(grid.scales.copy()))
+
+
+def cwth_decimate(signal: SignalBuffer, grid: ScaleGrid, params: MorletParams | None = None,
+                  hop: int = 128, anti_alias: bool = False, *, threads: int = 1, device=None,
+                  engine: str = "auto") -> CoefficientMatrix:
+    """Drop-in for wavelet.py:276-294: decimate by ``hop`` (signal_io.py:130-150, optional
+    anti-alias FIR) on the device, then the full hop = 1 transform of the decimated signal
+    -- the scales act on the decimated rate.  Returns the reference's matrix: hop = ``hop``,
+    source_rate = rate / hop."""
+    params = params or MorletParams()
+    hop = _check_hop(hop)
+    vals = cwth_decimate_batch(signal.samples.astype(np.float32)[None, :], grid.scales, params,
+                               hop, anti_alias, wavelet="cmor", output="complex", device=device,
+                               engine=engine)[0]
+    return CoefficientMatrix(vals.astype(np.complex128), hop, signal.sample_rate / hop,
+                             ScaleGrid(grid.scales.copy()))
+
+
+def cwth_decimate_batch(x, scales, params: MorletParams | None = None, hop: int = 128,
+                        anti_alias: bool = False, *, wavelet: str = "cmor",
+                        output: str = "complex", norm=None, device=None, engine: str = "auto"):
+    """Batched cwth_decimate: host float32 [B, N] -> (B, S, ceil(N/hop)) on the device
+    (wh_decimate, then a hop-1 plan on the decimated clips; nothing leaves the GPU between
+    the two)."""
+    import torch
+
+    from .signal_io import decimate_device
+
+    hop = _check_hop(hop)
+    arr = np.asarray(x, dtype=np.float32)
+    xx = np.atleast_2d(arr)
+    dev = torch.device("cuda", _device_index(device))
+    xd = torch.from_numpy(np.ascontiguousarray(xx)).to(dev)
+    dec = decimate_device(xd, hop, anti_alias)
+    plan = get_plan(scales, params, 1, dec.shape[1], wavelet=wavelet, output=output, norm=norm,
+                    clips=dec.shape[0], device=dev.index, engine=engine)
+    res = plan.execute(dec).cpu().numpy()
+    return res if arr.ndim == 2 else res[0]
 
 
 def cwt_fft(signal: SignalBuffer, grid: ScaleGrid, params: MorletParams | None = None, *,

@@ -67,3 +67,13 @@ def built_lib():
     from paper_2408_14302_b200 import build
 
     return build.build()
+
+
+@pytest.fixture(scope="session")
+def golden_formats():
+    return np.load(os.path.join(GOLDEN, "formats.npz"))
+
+
+def decimate_cases(g, prefix):
+    names = sorted({k.split("__")[0] for k in g.files if k.startswith(prefix) and "__" in k})
+    return [(n, {k.split("__")[1]: g[k] for k in g.files if k.startswith(n + "__")}) for n in names]

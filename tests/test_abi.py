@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol(built_lib):
 
 
 def test_abi_version(built_lib):
-    assert _lib.load().wh_abi_version() == 1
+    assert _lib.load().wh_abi_version() == 2
 
 
 def test_half_width_matches_oracle(built_lib):
