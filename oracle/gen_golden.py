@@ -167,6 +167,29 @@ def main():
         for ext in ("scg1", "pgm", "csv"):
             with open(os.path.join(td, f"m.{ext}"), "rb") as f:
                 fmt[f"file_{ext}"] = np.frombuffer(f.read(), dtype=np.uint8)
+    # wav / synth (signal_io.py:63-250) for the CLI and scan rows
+    from wavehop.signal_io import read_wav, write_wav  # noqa: E402
+    import struct  # noqa: E402
+    for i, (kind, kw) in enumerate((("impulse", dict(position=17)), ("sine", dict(frequency=440.0, amplitude=0.3)),
+                                    ("chirp", dict(f0=100.0, f1=3000.0)), ("white_noise", dict(seed=7)))):
+        fmt[f"synth_{kind}"] = synthesize(SynthSpec(kind, 1000, 8000.0, **kw)).samples
+    sig = SignalBuffer(np.sin(np.arange(300) * 0.05) * 0.9, 11025.0)
+    with tempfile.TemporaryDirectory() as td:
+        for enc in ("pcm16", "float32"):
+            write_wav(sig, os.path.join(td, f"{enc}.wav"), encoding=enc)
+            with open(os.path.join(td, f"{enc}.wav"), "rb") as f:
+                fmt[f"wav_{enc}"] = np.frombuffer(f.read(), dtype=np.uint8)
+            fmt[f"wav_{enc}__read"] = read_wav(os.path.join(td, f"{enc}.wav")).samples
+        # a stereo pcm16 file with an odd-sized extra chunk (word alignment) -> mono average
+        st = (np.arange(40, dtype=np.int16).reshape(20, 2) * np.array([100, -37], dtype=np.int16)).tobytes()
+        fmtc = struct.pack("<HHIIHH", 1, 2, 22050, 22050 * 4, 4, 16)
+        body = b"WAVE" + b"fmt " + struct.pack("<I", 16) + fmtc + b"LIST" + struct.pack("<I", 3) + b"abc\x00"
+        body += b"data" + struct.pack("<I", len(st)) + st
+        blob = b"RIFF" + struct.pack("<I", len(body)) + body
+        with open(os.path.join(td, "st.wav"), "wb") as f:
+            f.write(blob)
+        fmt["wav_stereo"] = np.frombuffer(blob, dtype=np.uint8)
+        fmt["wav_stereo__read"] = read_wav(os.path.join(td, "st.wav")).samples
     np.savez_compressed(os.path.join(OUT, "formats.npz"), **fmt)
     for f in ("taps.npz", "cwth.npz", "formats.npz"):
         print(f, os.path.getsize(os.path.join(OUT, f)), "bytes")

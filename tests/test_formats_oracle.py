@@ -93,3 +93,47 @@ def test_read_matrix_bin_errors(tmp_path):
         S.read_matrix_bin(p)
     with pytest.raises(wh.IoFailure):
         S.read_matrix_bin(tmp_path / "missing.scg1")
+
+
+def test_synth_and_wav_match_reference(golden_formats, tmp_path):
+    from paper_2408_14302_b200 import wavio
+
+    g = golden_formats
+    specs = (("impulse", dict(position=17)), ("sine", dict(frequency=440.0, amplitude=0.3)),
+             ("chirp", dict(f0=100.0, f1=3000.0)), ("white_noise", dict(seed=7)))
+    for kind, kw in specs:
+        np.testing.assert_array_equal(wavio.synthesize(wavio.SynthSpec(kind, 1000, 8000.0, **kw)).samples,
+                                      g[f"synth_{kind}"])
+    sig = wh.SignalBuffer(np.sin(np.arange(300) * 0.05) * 0.9, 11025.0)
+    for enc in ("pcm16", "float32"):
+        wavio.write_wav(sig, tmp_path / f"{enc}.wav", encoding=enc)
+        assert (tmp_path / f"{enc}.wav").read_bytes() == g[f"wav_{enc}"].tobytes()
+        np.testing.assert_array_equal(wavio.read_wav(tmp_path / f"{enc}.wav").samples, g[f"wav_{enc}__read"])
+    (tmp_path / "st.wav").write_bytes(g["wav_stereo"].tobytes())
+    st = wavio.read_wav(tmp_path / "st.wav")
+    np.testing.assert_array_equal(st.samples, g["wav_stereo__read"])
+    assert st.sample_rate == 22050.0
+    (tmp_path / "bad.wav").write_bytes(b"RIFF\x00\x00\x00\x00WAVX")
+    with pytest.raises(wh.MalformedRiff):
+        wavio.read_wav(tmp_path / "bad.wav")
+    with pytest.raises(wh.InvalidSpec):
+        wavio.SynthSpec("sine", 10, 8000.0, frequency=5000.0)
+
+
+def test_cli_parsing_and_errors(tmp_path, capsys):
+    from paper_2408_14302_b200 import cli
+
+    spec = cli.parse_synth_spec("sine:frequency=1000,amplitude=0.5", 100, 16000.0)
+    assert spec.kind == "sine" and spec.frequency == 1000.0 and spec.amplitude == 0.5
+    assert cli.parse_synth_spec("noise:seed=3", 10, 8000.0).kind == "white_noise"
+    with pytest.raises(wh.InvalidSpec):
+        cli.parse_synth_spec("sine:frequency", 10, 8000.0)
+    with pytest.raises(wh.InvalidSpec):
+        cli.parse_synth_spec("sine:colour=red", 10, 8000.0)
+    assert cli.run_cli([]) == 2  # usage error
+    assert cli.run_cli(["scan", str(tmp_path), "--out-dir", str(tmp_path / "o")]) == 1
+    assert "no .wav files" in capsys.readouterr().err
+    assert cli.run_cli(["synth", "sine:frequency=440", "--out", str(tmp_path / "s.wav"),
+                        "--length", "64", "--rate", "8000"]) == 0
+    assert (tmp_path / "s.wav").stat().st_size == 44 + 128
+    assert cli.run_cli(["scalogram", str(tmp_path / "missing.scg1"), "--out", str(tmp_path / "x.pgm")]) == 1
