@@ -200,7 +200,7 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
     cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
     cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow);
-    cudaFree(p->d_minmax); cudaFree(p->d_scratch); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
+    cudaFree(p->d_minmax); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     cudaSetDevice(cur);
@@ -268,9 +268,10 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
         if (cudaMalloc(&p->d_minmax, sizeof(uint32_t) * 2 * max_clips) != cudaSuccess)
             rc = fail(WH_E_OOM, "cudaMalloc(minmax) failed");
     }
-    if (rc == WH_OK && is_render(*p)) {  // float values before the uint8 map
-        if (cudaMalloc(&p->d_scratch, sizeof(float) * (size_t)max_clips * n_scales * p->F) != cudaSuccess)
-            rc = fail(WH_E_OOM, "cudaMalloc(render scratch) failed");
+    if (rc == WH_OK && is_render(*p)) {  // float values before the uint8 map + map parameters
+        if (cudaMalloc(&p->d_scratch, sizeof(float) * (size_t)max_clips * n_scales * p->F) != cudaSuccess ||
+            cudaMalloc(&p->d_rparams, (size_t)WH_RENDER_PARAM_BYTES * max_clips) != cudaSuccess)
+            rc = fail(WH_E_OOM, "cudaMalloc(render workspace) failed");
     }
     std::string why;
     if (rc == WH_OK) {
@@ -333,7 +334,8 @@ int wh_plan_out_bytes(const wh_plan *plan, int64_t clips, int64_t *bytes) {
 int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches) {
     if (!plan || !launches) return fail(WH_E_INVALID_ARG, "NULL argument");
     const Plan *p = reinterpret_cast<const Plan *>(plan);
-    *launches = clips > 0 ? (1 + (p->norm != WH_NORM_NONE ? 2 : 0)) : 0;
+    // engine + (min/max reset + normalise) or (reset + map parameters + uint8 map)
+    *launches = clips > 0 ? (1 + (p->norm == WH_NORM_MINMAX ? 2 : 0) + (is_render(*p) ? 3 : 0)) : 0;
     return WH_OK;
 }
 
@@ -366,7 +368,7 @@ int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im,
 // mm: this call's slice of the per-clip min/max keys; scratch: its slice of the float
 // values a render plan maps to uint8
 static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev, cudaStream_t s,
-                        uint32_t *mm, float *scratch) {
+                        uint32_t *mm, float *scratch, void *rparams) {
     int rc = WH_OK;
     const bool render = is_render(*p);
     void *dst = render ? static_cast<void *>(scratch) : out_dev;
@@ -376,7 +378,7 @@ static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x
                                            : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm);
     if (rc == WH_OK && p->norm == WH_NORM_MINMAX) rc = minmax_apply(*p, clips, out_dev, mm, s);
     if (rc == WH_OK && render)
-        rc = render_apply(scratch, clips, p->S, p->F, mm, p->norm == WH_NORM_RENDER_U8 ? 1 : 0,
+        rc = render_apply(scratch, clips, p->S, p->F, mm, rparams, p->norm == WH_NORM_RENDER_U8 ? 1 : 0,
                           static_cast<uint8_t *>(out_dev), s);
     return rc;
 }
@@ -393,7 +395,7 @@ int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, v
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != p->device) WH_CUDA_TRY(cudaSetDevice(p->device));
-    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax, p->d_scratch);
+    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax, p->d_scratch, p->d_rparams);
     if (prev != p->device) cudaSetDevice(prev);
     return rc;
 }
@@ -451,7 +453,9 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
             break;
         }
         rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0,
-                          p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr);
+                          p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr,
+                          p->d_rparams ? static_cast<uint8_t *>(p->d_rparams) + (size_t)WH_RENDER_PARAM_BYTES * c0
+                                       : nullptr);
         if (rc == WH_OK && cudaMemcpyAsync(reinterpret_cast<uint8_t *>(out_host) + (size_t)c0 * out_clip, dout,
                                            (size_t)nc * out_clip, cudaMemcpyDeviceToHost, s) != cudaSuccess)
             rc = fail(WH_E_CUDA, "D2H copy failed");

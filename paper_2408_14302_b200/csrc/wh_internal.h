@@ -123,6 +123,7 @@ struct Plan {
     // per-clip min/max (ordered-uint keys) for WH_NORM_MINMAX
     uint32_t *d_minmax = nullptr;  // [max_clips][2]
     float *d_scratch = nullptr;    // render plans: float values [max_clips][S][F] before the uint8 map
+    void *d_rparams = nullptr;     // render plans: WH_RENDER_PARAM_BYTES per clip
 
     // host staging for wh_execute_host
     float *d_x = nullptr;
@@ -145,8 +146,9 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
 
 // epilogue helpers (wh_api.cu)
 int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, cudaStream_t s);
-int render_apply(const float *values, int64_t clips, int64_t rows, int64_t cols, const uint32_t *mm, int32_t flip,
-                 uint8_t *out, cudaStream_t s);
+constexpr int WH_RENDER_PARAM_BYTES = 24;  // per-matrix affine map of render_apply
+int render_apply(const float *values, int64_t clips, int64_t rows, int64_t cols, const uint32_t *mm, void *params,
+                 int32_t flip, uint8_t *out, cudaStream_t s);
 inline bool is_render(const Plan &p) { return p.norm == WH_NORM_RENDER_U8 || p.norm == WH_NORM_RENDER_U8_NOFLIP; }
 int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s);
 
