@@ -838,11 +838,38 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
         if (A.conv_regs) {
-            // Register-prefetch path (no staging buffer): each thread loads its <= CONV_RC
+            // Register-prefetch path (no staging buffer): each thread loads its first CONV_RC
             // chunks of the next window into registers while the MMAs of the previous unit
-            // run, then converts from registers once the window buffer is free.
+            // run, then converts from registers once the window buffer is free.  Larger
+            // windows (c5: 13.5 chunks per thread) read their extra chunks twice: once
+            // before the wait for the window max, again (L2 hits) after it.
             constexpr int CONV_RC = 10;
             const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
+            auto load8 = [&](const float *xb, int64_t w0, int32_t off, int32_t in_lo, int32_t in_hi, float (&o)[8]) {
+                if (A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
+                    const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
+                    const float4 u = __ldg(g), w = __ldg(g + 1);
+                    o[0] = u.x; o[1] = u.y; o[2] = u.z; o[3] = u.w;
+                    o[4] = w.x; o[5] = w.y; o[6] = w.z; o[7] = w.w;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int32_t q = off + k;
+                        o[k] = (q >= in_lo && q < in_hi) ? __ldg(xb + w0 + q) : 0.0f;
+                    }
+                }
+            };
+            auto split8 = [&](const float (&in)[8], float sc, uint32_t (&hw)[4], uint32_t (&lw)[4]) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 a2 = make_float2(in[2 * k] * sc, in[2 * k + 1] * sc);
+                    const __half2 h = __float22half2_rn(a2);
+                    const float2 hf = __half22float2(h);
+                    const __half2 l = __float22half2_rn(make_float2(a2.x - hf.x, a2.y - hf.y));
+                    hw[k] = *reinterpret_cast<const uint32_t *>(&h);
+                    lw[k] = *reinterpret_cast<const uint32_t *>(&l);
+                }
+            };
             uint32_t wcnt = 0;
             for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
                 int64_t b, tile;
@@ -856,22 +883,23 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 if (ct == 0) WH_TRACE(3, wcnt);
                 float v[CONV_RC][8];
                 float mx = 0.0f;
+                auto chunk_off = [&](int c) { return (int32_t)((c >> cpr_shift) * A.V + (c & cpr_mask) * 8); };
 #pragma unroll
                 for (int i = 0; i < CONV_RC; ++i) {
                     const int c = ct + i * UM_CONV_THREADS;
-                    const int32_t off = (c >> cpr_shift) * A.V + (c & cpr_mask) * 8;
-                    if (c < chunks && A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
-                        const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
-                        const float4 u = __ldg(g), w = __ldg(g + 1);
-                        v[i][0] = u.x; v[i][1] = u.y; v[i][2] = u.z; v[i][3] = u.w;
-                        v[i][4] = w.x; v[i][5] = w.y; v[i][6] = w.z; v[i][7] = w.w;
+                    if (c < chunks) {
+                        load8(xb, w0, chunk_off(c), in_lo, in_hi, v[i]);
                     } else {
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const int32_t o = off + k;
-                            v[i][k] = (c < chunks && o >= in_lo && o < in_hi) ? __ldg(xb + w0 + o) : 0.0f;
-                        }
+                        for (int k = 0; k < 8; ++k) v[i][k] = 0.0f;
                     }
+                }
+                // chunks beyond the register share: max only (re-read after the wait)
+                for (int c = ct + CONV_RC * UM_CONV_THREADS; c < chunks; c += UM_CONV_THREADS) {
+                    float t[8];
+                    load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(t[k]));
                 }
 #pragma unroll
                 for (int i = 0; i < CONV_RC; ++i)
@@ -894,39 +922,44 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 // while the window buffer is still busy; only the stores wait for it
 #pragma unroll
                 for (int i = 0; i < CONV_RC; ++i) {
-                    uint32_t w[8];
+                    uint32_t hw[4], lw[4];
+                    split8(v[i], sc, hw, lw);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const float2 a = make_float2(v[i][2 * k] * sc, v[i][2 * k + 1] * sc);
-                        const __half2 h = __float22half2_rn(a);
-                        const float2 hf = __half22float2(h);
-                        const __half2 l = __float22half2_rn(make_float2(a.x - hf.x, a.y - hf.y));
-                        w[k] = *reinterpret_cast<const uint32_t *>(&h);
-                        w[4 + k] = *reinterpret_cast<const uint32_t *>(&l);
+                        v[i][k] = __uint_as_float(hw[k]);
+                        v[i][4 + k] = __uint_as_float(lw[k]);
                     }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) v[i][k] = __uint_as_float(w[k]);
                 }
                 if (ct == 0) WH_TRACE(5, wcnt);
                 mbar_wait_p(&win_empty[wb], ((wcnt / A.win_bufs) & 1) ^ 1, pa, 1, pon);
                 if (ct == 0) WH_TRACE(6, wcnt);
                 uint8_t *whi = win_base + (size_t)wb * 2 * WH;
                 uint8_t *wlo = whi + WH;
+                auto put = [&](int c, const uint32_t (&hw)[4], const uint32_t (&lw)[4]) {
+                    const int row = c >> cpr_shift, cc = c & cpr_mask;
+                    const int panel = cc >> 3, c8 = cc & 7;
+                    const uint32_t off =
+                        (uint32_t)panel * panel_bytes + (uint32_t)row * 128u + (uint32_t)((c8 ^ (row & 7)) * 16);
+                    *reinterpret_cast<uint4 *>(whi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    *reinterpret_cast<uint4 *>(wlo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                };
 #pragma unroll
                 for (int i = 0; i < CONV_RC; ++i) {
                     const int c = ct + i * UM_CONV_THREADS;
                     if (c < chunks) {
-                        const int row = c >> cpr_shift, cc = c & cpr_mask;
-                        const int panel = cc >> 3, c8 = cc & 7;
-                        const uint32_t off = (uint32_t)panel * panel_bytes + (uint32_t)row * 128u +
-                                             (uint32_t)((c8 ^ (row & 7)) * 16);
-                        *reinterpret_cast<uint4 *>(whi + off) =
-                            make_uint4(__float_as_uint(v[i][0]), __float_as_uint(v[i][1]), __float_as_uint(v[i][2]),
-                                       __float_as_uint(v[i][3]));
-                        *reinterpret_cast<uint4 *>(wlo + off) =
-                            make_uint4(__float_as_uint(v[i][4]), __float_as_uint(v[i][5]), __float_as_uint(v[i][6]),
-                                       __float_as_uint(v[i][7]));
+                        const uint32_t hw[4] = {__float_as_uint(v[i][0]), __float_as_uint(v[i][1]),
+                                                __float_as_uint(v[i][2]), __float_as_uint(v[i][3])};
+                        const uint32_t lw[4] = {__float_as_uint(v[i][4]), __float_as_uint(v[i][5]),
+                                                __float_as_uint(v[i][6]), __float_as_uint(v[i][7])};
+                        put(c, hw, lw);
                     }
+                }
+                for (int c = ct + CONV_RC * UM_CONV_THREADS; c < chunks; c += UM_CONV_THREADS) {
+                    float t[8];
+                    uint32_t hw[4], lw[4];
+                    load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
+                    split8(t, sc, hw, lw);
+                    put(c, hw, lw);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (ct == 0) xring[wcnt & 3] = ldexpf(1.0f, -ex);
@@ -1347,7 +1380,10 @@ int umma_prepare(Plan &p) {
         const int64_t ksteps = (G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1;
         double cost = 0.0;
         // heavy (long-tap) passes first so the accumulator pipeline starts on the long ones
-        for (int s0 = ((p.S - 1) / spp) * spp; s0 >= 0; s0 -= spp) {
+        // (alternating heavy / light passes measured no better on c5)
+        std::vector<int> order;
+        for (int s0 = ((p.S - 1) / spp) * spp; s0 >= 0; s0 -= spp) order.push_back(s0);
+        for (int s0 : order) {
             UmmaPass ps{};
             ps.s0 = s0;
             ps.ns = std::min(spp, p.S - s0);
@@ -1672,7 +1708,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.res_bytes = (uint32_t)p.res_bytes;
     a.n_stream = p.n_stream;
     a.cpr_shift = p.panels == 1 ? 3 : p.panels == 2 ? 4 : p.panels == 4 ? 5 : -1;
-    a.conv_regs = (!p.use_stg && (int64_t)p.win_rows * p.panels * 8 <= 10 * 128 && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
+    a.conv_regs = (!p.use_stg && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;

@@ -40,23 +40,25 @@ def cwth_multi_device(x: np.ndarray, scales, params=None, hop: int = 128, *, dev
     x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float32)
     B, n = x.shape
     devices = list(devices)
-    plans = {}
     ranges = [shard_range(B, len(devices), r) for r in range(len(devices))]
-    for d, (a, b) in zip(devices, ranges):
-        if b > a:
-            plans[d] = CwthPlan(scales, params, hop, n, wavelet=wavelet, output=output, norm=norm,
-                                max_clips=b - a, device=d, engine=engine)
-    frames = next(iter(plans.values())).frames if plans else -(-n // hop)
-    out = np.empty((B, len(scales), frames), dtype=np.complex64 if output == "complex" else np.float32)
+    # one plan per SHARD (a plan's staging buffers serve one host thread at a time, and the
+    # same device may appear twice in ``devices``)
+    plans = {r: CwthPlan(scales, params, hop, n, wavelet=wavelet, output=output, norm=norm,
+                         max_clips=b - a, device=d, engine=engine)
+             for r, (d, (a, b)) in enumerate(zip(devices, ranges)) if b > a}
+    first = next(iter(plans.values()), None)
+    frames = first.frames if first else -(-n // hop)
+    dtype = first.out_dtype if first else (np.complex64 if output == "complex" else np.float32)
+    out = np.empty((B, len(scales), frames), dtype=dtype)
     errors = []
 
-    def run(d, a, b):
+    def run(r, a, b):
         try:
-            plans[d].execute_host(x[a:b], out=out[a:b])
+            plans[r].execute_host(x[a:b], out=out[a:b])
         except Exception as e:  # noqa: BLE001
             errors.append(e)
 
-    threads = [threading.Thread(target=run, args=(d, a, b)) for d, (a, b) in zip(devices, ranges) if b > a]
+    threads = [threading.Thread(target=run, args=(r, a, b)) for r, (a, b) in enumerate(ranges) if b > a]
     for t in threads:
         t.start()
     for t in threads:

@@ -1,1 +1,2 @@
-for e in "WH_UMMA_GROUP_KB=48" "WH_UMMA_GROUP_KB=24" "WH_UMMA_GROUP_KB=16" "WH_UMMA_GROUP_KB=24 WH_UMMA_SMEM_OPT=1"; do echo "== $e"; env $e WH_UMMA_VERBOSE=1 timeout 120 python tools/trace_units.py --config c5 --clips 148 2>&1 | grep -E "wh umma|^   [23] |CTA 0" | cut -c1-60,150-400; env $e timeout 200 python bench.py --config c5 --clips 296 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], '%.4f ms' % d['ms_per_step'], '%.3e' % d['value'], d['clocks']['sm_mhz'])"; done
+timeout 600 python -m pytest tests -q -m gpu 2>&1 | tail -2
+for i in 1 2 3; do timeout 600 python -m pytest tests -q -m gpu -k "sharded or host_paths" 2>&1 | tail -1; done
