@@ -310,3 +310,26 @@ def test_seam2_kernels_match_oracle():
         r = O.strided_correlate_symmetric(xpad, even, odd, hop, frames)
         sc = max(np.abs(r[0]).max(), np.abs(r[1]).max())
         assert np.abs(ore - r[0]).max() <= 1e-12 * sc and np.abs(oim - r[1]).max() <= 1e-12 * sc
+
+
+@pytest.mark.parametrize("env", [{"WH_UMMA_HYBRID": "1"}, {"WH_UMMA_NO_RESIDENT": "1"},
+                                 {"WH_UMMA_CG1": "1"}, {"WH_UMMA_TAU": "0"},
+                                 {"WH_UMMA_NO_CONVREGS": "1"}, {"WH_UMMA_G0_ALIGN": "64"}])
+def test_umma_planner_variants_agree(env, monkeypatch):
+    """Every planner / kernel variant the diagnostics switches select (resident + streamed
+    hybrid bank, fully streamed bank, single-CTA MMAs, no tail skipping, staged converter,
+    another K origin) computes the same transform within tolerance (c2 and c5 shapes)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for cid, hop, wavelet, output in ((2, 64, "rmor", "log1p"), (5, 32, "cmor", "abs")):
+        x = synth.make_batch(cid, clips=2, n=30000, start=4)
+        sc = synth.config_scales(cid)
+        plan = wh.CwthPlan(sc, None, hop, 30000, wavelet=wavelet, output=output, max_clips=2,
+                           engine="umma")
+        got = plan.execute_host(x)
+        plan.close()
+        ref = O.cwth_batch(x, sc, hop, wavelet=wavelet, output=output)
+        if output == "log1p":
+            assert np.abs(got - ref).max() <= 1e-5, env
+        else:
+            assert row_rel_err(got, ref) <= ROW_TOL, env
