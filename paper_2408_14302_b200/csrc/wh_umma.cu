@@ -51,7 +51,6 @@ static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
 struct UmmaArgs {
     const float *x;
     int64_t ld_x, N, F, hop;
-    int64_t items;              // clips * row_tiles
     int64_t clips;
     int32_t row_tiles, V, P, Cc, panels, G0, win_rows, S;
     int32_t rs;                         // rows per frame (hop = 256 * rs > 256), else 1
@@ -1316,7 +1315,8 @@ int umma_supported(const Plan &p, std::string *why) {
     return WH_OK;
 }
 
-// compact smem tile format: k < 2^16, c0 and ncols < 2^8, byte_off multiple of 256
+// compact smem tile format (s_tile): 16-byte descriptor offsets, c0 and ncols < 2^8, tiles
+// 128-byte aligned in the bank
 static int ncheck_tiles(const Plan &p) {
     for (auto &t : p.tiles)
         if ((int64_t)t.k * 64 / p.V >= 4096 || p.V / 64 > 16 || t.c0 > 255 || t.ncols > 255 || (t.byte_off & 127))
@@ -1338,10 +1338,6 @@ int umma_prepare(Plan &p) {
         H = 256;
     }
     p.V = (int32_t)(H <= 64 ? 64 : H);
-    if (const char *vm = std::getenv("WH_UMMA_VMUL")) {  // diagnostics: rows of V * vmul samples
-        const int vmul = std::atoi(vm);
-        if ((vmul == 2 || vmul == 4) && p.rs == 1) p.V = std::min<int32_t>(p.V * vmul, 256);
-    }
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
     p.panels = p.V / 64;
@@ -1697,7 +1693,6 @@ int umma_prepare(Plan &p) {
 int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm) {
     UmmaArgs a{};
     a.x = x; a.ld_x = ld_x; a.N = p.N; a.F = p.F; a.hop = p.hop;
-    a.items = clips * p.row_tiles;
     a.row_tiles = p.row_tiles; a.V = p.V; a.P = p.P; a.Cc = p.Cc; a.panels = p.panels; a.rs = p.rs;
     a.G0 = p.G0; a.win_rows = p.win_rows; a.S = p.S;
     a.n_passes = (int32_t)p.passes.size(); a.n_tiles = (int32_t)p.tiles.size();
@@ -1713,11 +1708,8 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
     a.minmax = p.norm != WH_NORM_NONE ? mm : nullptr;
-    int max_cols = 16;
-    for (auto &t : p.tiles) max_cols = std::max(max_cols, t.ncols);
     a.clips = clips;
     a.ring_bytes = (uint32_t)p.ring_bytes;
-    (void)max_cols;
     a.win_half_bytes = (uint32_t)p.panels * (uint32_t)p.win_rows * 128u;
     a.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (p.F % 4 == 0);
     a.prof = p.d_prof;

@@ -333,3 +333,19 @@ def test_umma_planner_variants_agree(env, monkeypatch):
             assert np.abs(got - ref).max() <= 1e-5, env
         else:
             assert row_rel_err(got, ref) <= ROW_TOL, env
+
+
+@pytest.mark.parametrize("engine", ["umma", "simt"])
+def test_unaligned_rows_and_odd_lengths(engine):
+    """ld_x not a multiple of 4 (no 16-byte vector loads) and N not a multiple of the hop:
+    same values as the packed layout."""
+    rng = np.random.default_rng(21)
+    n, ld = 10001, 10004 + 3
+    base = rng.standard_normal((3, ld)).astype(np.float32)
+    sc = np.geomspace(1.0, 40.0, 12)
+    plan = wh.CwthPlan(sc, None, 16, n, wavelet="cmor", output="complex", max_clips=3, engine=engine)
+    xt = torch.from_numpy(base).cuda()[:, 1:1 + n]  # offset view: rows not 16-byte aligned
+    got = plan.execute(xt).cpu().numpy()
+    ref = O.cwth_batch(base[:, 1:1 + n], sc, 16, output="complex")
+    assert got.shape == ref.shape == (3, 12, -(-n // 16))
+    assert row_rel_err(got, ref) <= ROW_TOL

@@ -1,2 +1,1 @@
-for c in c1 c2 c3 c4h1 c4h16 c4h64 c4h256 c4h1024; do timeout 200 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(d['config']['workload'], d['config']['engine'], '%.4f ms' % d['ms_per_step'], '%.3e' % d['value'], r['bound'], '%.3f' % r['frac'], 'tensor %.3f' % r['tensor_view']['frac'], 'hbm %.3f' % r['hbm_view']['frac'])"; done
-timeout 300 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 > gpurun_out/bench_c5_r01d.json; python -c "import json; d=json.loads(open('gpurun_out/bench_c5_r01d.json').read()); r=d['roofline']; print('c5 full', '%.3f ms' % d['ms_per_step'], '%.3e' % d['value'], r['bound'], '%.3f' % r['frac'], 'kernel %.3f ms' % r['kernel_ms'], 'e2e %.3e' % d['e2e']['value'], d['clocks'])"
+timeout 600 python -m pytest tests -q -m gpu -k "unaligned" 2>&1 | tail -5
