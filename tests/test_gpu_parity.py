@@ -349,3 +349,19 @@ def test_unaligned_rows_and_odd_lengths(engine):
     ref = O.cwth_batch(base[:, 1:1 + n], sc, 16, output="complex")
     assert got.shape == ref.shape == (3, 12, -(-n // 16))
     assert row_rel_err(got, ref) <= ROW_TOL
+
+
+def test_long_signal_and_empty_batch():
+    """A 5M-sample clip (sample offsets far beyond 2^16 tiles of rows) and a zero-clip call."""
+    rng = np.random.default_rng(33)
+    n = 5_000_000
+    x = rng.standard_normal((1, n)).astype(np.float32)
+    sc = [1.0, 3.0, 9.0, 27.0]
+    for hop, engine in ((64, "umma"), (1024, "umma"), (7, "simt")):
+        got = wh.cwth_batch(x, sc, None, hop, wavelet="cmor", output="abs", engine=engine)
+        ref = O.cwth_batch(x, sc, hop, wavelet="cmor", output="abs")
+        assert got.shape == ref.shape == (1, 4, -(-n // hop))
+        assert row_rel_err(got, ref) <= ROW_TOL, (hop, engine)
+    plan = wh.CwthPlan(sc, None, 64, 1000, max_clips=2)
+    empty = plan.execute(torch.empty((0, 1000), dtype=torch.float32, device="cuda"))
+    assert tuple(empty.shape) == (0, 4, 16)

@@ -1,3 +1,1 @@
-for t in 12 8; do echo "== TAU $t"; WH_UMMA_TAU=$t timeout 60 python tools/gpu_check.py umma 2>&1 | grep -E "c2s|c3s|c4s_h16|c5s|impulse"; WH_UMMA_TAU=$t timeout 600 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
-for c in c2 c4h16; do WH_UMMA_TAU=$t timeout 200 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], '%.4f ms' % d['ms_per_step'])"; done
-WH_UMMA_TAU=$t timeout 200 python bench.py --config c5 --clips 296 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], '%.4f ms' % d['ms_per_step'])"; done
+timeout 600 python -m pytest tests -q -m gpu -k "long_signal" 2>&1 | tail -5
