@@ -73,7 +73,10 @@ struct UmmaArgs {
     uint32_t ring_bytes, win_half_bytes;
     int32_t out_vec_ok;             // output base 16B aligned and F % 4 == 0
     unsigned long long *prof;       // optional per-role wait counters (wh_plan_profile)
-    int32_t dbg;                    // diagnostics: 1 no epilogue work, 2 no converter work, 4 no MMA
+    int32_t dbg;                    // diagnostics (WH_UMMA_DBG bits, results invalid): 1 no epilogue work,
+                                    // 2 no converter work, 4 no MMA, 8 cluster-scope window release,
+                                    // 32 no output stores, 64 no accumulator re-zeroing,
+                                    // 128 no streamed tap copies after the first unit
     long long *trace;               // diagnostics: CTA-0 timeline [event][unit] (WH_UMMA_TRACE)
 };
 
@@ -684,9 +687,13 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     const long long t_issue = pon ? clock64() : 0;
                     if (elect_one()) {
                         s_vstart[slot] = v;
-                        mbar_expect_tx(&b_full[slot], bytes);
-                        bulk_g2s(ring_base + phys, A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * bytes, bytes,
-                                 &b_full[slot]);
+                        if ((A.dbg & 128) && item != u0) {
+                            mbar_arrive(&b_full[slot]);  // diagnostics: stale taps, no L2 traffic
+                        } else {
+                            mbar_expect_tx(&b_full[slot], bytes);
+                            bulk_g2s(ring_base + phys, A.bank + ((size_t)(uint32_t)gr.z << 7) + (size_t)rank * bytes,
+                                     bytes, &b_full[slot]);
+                        }
                     }
                     __syncwarp();
                     if (pon) pa.c[1] += (unsigned long long)(clock64() - t_issue);
