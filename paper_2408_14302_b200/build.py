@@ -39,15 +39,31 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB, *sources()]
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = os.path.join(HERE, "csrc", "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    procs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        procs.append((src, obj, subprocess.Popen([NVCC, *cflags, "-c", "-o", obj, src],
+                                                 stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log = []
+    for src, obj, pr in procs:
+        out, err = pr.communicate()
+        log.append(err)
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(src)}")
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *[o for _, o, _ in procs]]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
-        raise RuntimeError("nvcc failed building libwavehop_b200.so")
+        raise RuntimeError("nvcc failed linking libwavehop_b200.so")
     if verbose:
-        sys.stderr.write(proc.stderr)
+        sys.stderr.write("".join(log))
     with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
-        f.write(proc.stderr)
+        f.write("".join(log))
     return LIB
 
 

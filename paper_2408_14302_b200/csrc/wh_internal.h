@@ -106,6 +106,8 @@ struct Plan {
     uint8_t *d_bank = nullptr;
     int64_t bank_bytes = 0;
     float *d_scale_pow = nullptr;  // per scale 2^-f_s
+    uint8_t *d_tables = nullptr;   // UMMA: the kernel's smem tables, packed (one bulk copy)
+    int64_t tables_bytes = 0;
     std::vector<int32_t> fexp;
     int32_t bstages = 2, win_bufs = 2;     // bstages: full-width tiles the ring holds (info)
     int64_t ring_bytes = 0;                // tap-tile ring capacity

@@ -68,6 +68,8 @@ struct UmmaArgs {
     int32_t n_groups;
     const uint8_t *bank;
     const float *scale_pow;
+    const uint8_t *tables;          // packed smem tables (pass, group, tile, goff, spow), 16 B multiple
+    uint32_t tables_bytes;
     void *out;
     uint32_t *minmax;
     uint32_t ring_bytes, win_half_bytes;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     __shared__ __align__(8) uint64_t win_full[2], win_empty[2], acc_full[2], acc_empty[2];
     __shared__ float xring[4];  // per-unit window exponent 2^-e, written by the converters
     __shared__ float red[UM_CONV_WARPS];
-    __shared__ __align__(8) uint64_t stg_full, res_full;
+    __shared__ __align__(8) uint64_t stg_full, res_full, tab_full;
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -557,6 +559,62 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         b = u / tpu;
         tile = CG * (u % tpu) + rank;
     };
+    // Converters, register-prefetch path: each thread loads its first CONV_RC 8-sample chunks
+    // of a unit's window into registers (cv) and the window's max |x| over all its chunks
+    // (cmx).  The first unit's window is fetched right at launch, overlapping the setup.
+    constexpr int CONV_RC = 10;
+    float cv[CONV_RC][8];
+    float cmx = 0.0f;
+    auto conv_load8 = [&](const float *xb, int64_t w0, int32_t off, int32_t in_lo, int32_t in_hi, float (&o)[8]) {
+        if (A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
+            const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
+            const float4 u = __ldg(g), w = __ldg(g + 1);
+            o[0] = u.x; o[1] = u.y; o[2] = u.z; o[3] = u.w;
+            o[4] = w.x; o[5] = w.y; o[6] = w.z; o[7] = w.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int32_t q = off + k;
+                o[k] = (q >= in_lo && q < in_hi) ? __ldg(xb + w0 + q) : 0.0f;
+            }
+        }
+    };
+    auto conv_fetch = [&](int64_t item) {
+        int64_t b, tile;
+        unit_tile(item, b, tile);
+        const int64_t w0 = tile * 128 * A.V - A.G0;
+        const float *xb = A.x + b * A.ld_x;
+        const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);
+        const int64_t in_hi64 = A.N - w0;
+        const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
+        const int ct = (int)threadIdx.x - 64, chunks = A.win_rows * A.panels * 8;
+        const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
+        auto chunk_off = [&](int c) { return (int32_t)((c >> cpr_shift) * A.V + (c & cpr_mask) * 8); };
+#pragma unroll
+        for (int i = 0; i < CONV_RC; ++i) {
+            const int c = ct + i * UM_CONV_THREADS;
+            if (c < chunks) {
+                conv_load8(xb, w0, chunk_off(c), in_lo, in_hi, cv[i]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cv[i][k] = 0.0f;
+            }
+        }
+        float mx = 0.0f;
+        // chunks beyond the register share: max only (re-read after the wait)
+        for (int c = ct + CONV_RC * UM_CONV_THREADS; c < chunks; c += UM_CONV_THREADS) {
+            float t[8];
+            conv_load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(t[k]));
+        }
+#pragma unroll
+        for (int i = 0; i < CONV_RC; ++i)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(cv[i][k]));
+        cmx = mx;
+    };
+    if (warp >= 2 && warp < 2 + UM_CONV_WARPS && A.conv_regs && u0 < n_units) conv_fetch(u0);
     const uint32_t WH = A.win_half_bytes;               // bytes of one (hi or lo) window
     uint8_t *win_base = smem;                            // [win_bufs][hi|lo][panels][rows][128]
     uint8_t *stage_base = smem + (size_t)A.win_bufs * 2 * WH;
@@ -568,30 +626,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     uint4 *s_tile = reinterpret_cast<uint4 *>(s_group + A.n_groups);
     int *s_goff = reinterpret_cast<int *>(s_tile + A.n_tiles);  // resident: smem offset per group
     float *s_spow = reinterpret_cast<float *>(s_goff + A.n_groups);
-    for (int i = threadIdx.x; i < A.S; i += blockDim.x) s_spow[i] = A.scale_pow[i];
-    for (int i = threadIdx.x; i < A.n_passes; i += blockDim.x) {
-        const UmmaPass ps = A.passes[i];
-        s_pass[i] = make_int4(ps.group_begin, ps.group_end, ps.s0 | (ps.ns << 16), ps.cols);
+    // the tables arrive by one bulk copy (one HBM round trip at launch; the host packed them
+    // in their smem layout)
+    if (threadIdx.x == 0) {
+        mbar_init(&tab_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&tab_full, A.tables_bytes);
+        bulk_g2s(s_pass, A.tables, A.tables_bytes, &tab_full);
     }
-    for (int i = threadIdx.x; i < A.n_groups; i += blockDim.x) {
-        const UmmaGroup g = A.groups[i];
-        s_group[i] = make_int4(g.tile_begin, g.tile_end, (int)(uint32_t)(g.bank_off >> 7), g.cta_bytes);
-        s_goff[i] = g.pad_;
-    }
-    for (int i = threadIdx.x; i < A.n_tiles; i += blockDim.x) {
-        const UmmaTile tl = A.tiles[i];
-        // window row shift q and panel of this K-step's A operand (k*64 = q*V + panel*64)
-        const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)A.V, panel = (kg % (uint32_t)A.V) >> 6;
-        // pre-decoded MMA operands of the K-step, in 16-byte descriptor units:
-        //   x = A offset in the window | c0 << 16,   y = B offset in the group | B2 delta << 16,
-        //   z = instruction descriptor of MMA1 (N = nc + ncorr), w = of MMA2 (N = ncorr; 0 = none)
-        const uint32_t aoff = panel * (uint32_t)A.win_rows * 128u + q * 128u;
-        const uint32_t n1 = (uint32_t)(tl.ncols + tl.ncorr), n2 = (uint32_t)tl.ncorr;
-        const uint32_t b2d = (CG == 2 ? n1 / 2 : n1) * 128u;
-        s_tile[i] = make_uint4((aoff >> 4) | ((uint32_t)tl.c0 << 16), ((uint32_t)tl.in_off >> 4) | ((b2d >> 4) << 16),
-                               idesc_f16<CG>(n1), n2 ? idesc_f16<CG>(n2) : 0u);
-    }
-
     if (threadIdx.x == 0) {
         for (int i = 0; i < UM_SLOTS; ++i) {
             mbar_init(&b_full[i], (CG == 2 && leader) ? 2 : 1);  // + the peer's relay
@@ -621,6 +663,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    mbar_wait(&tab_full, 0);
     const uint32_t tmem = tmem_base_sh;
     if (warp >= 2 + UM_CONV_WARPS) {
         // epilogue warps zero both accumulator buffers of their lane quadrant: every MMA
@@ -849,22 +892,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             // run, then converts from registers once the window buffer is free.  Larger
             // windows (c5: 13.5 chunks per thread) read their extra chunks twice: once
             // before the wait for the window max, again (L2 hits) after it.
-            constexpr int CONV_RC = 10;
             const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
-            auto load8 = [&](const float *xb, int64_t w0, int32_t off, int32_t in_lo, int32_t in_hi, float (&o)[8]) {
-                if (A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
-                    const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
-                    const float4 u = __ldg(g), w = __ldg(g + 1);
-                    o[0] = u.x; o[1] = u.y; o[2] = u.z; o[3] = u.w;
-                    o[4] = w.x; o[5] = w.y; o[6] = w.z; o[7] = w.w;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int32_t q = off + k;
-                        o[k] = (q >= in_lo && q < in_hi) ? __ldg(xb + w0 + q) : 0.0f;
-                    }
-                }
-            };
+            auto load8 = conv_load8;
             auto split8 = [&](const float (&in)[8], float sc, uint32_t (&hw)[4], uint32_t (&lw)[4]) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -887,30 +916,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const int64_t in_hi64 = A.N - w0;
                 const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
                 if (ct == 0) WH_TRACE(3, wcnt);
-                float v[CONV_RC][8];
-                float mx = 0.0f;
+                // this unit's window (the first one was fetched at launch)
+                if (item != u0) conv_fetch(item);
+                float (&v)[CONV_RC][8] = cv;
+                float mx = cmx;
                 auto chunk_off = [&](int c) { return (int32_t)((c >> cpr_shift) * A.V + (c & cpr_mask) * 8); };
-#pragma unroll
-                for (int i = 0; i < CONV_RC; ++i) {
-                    const int c = ct + i * UM_CONV_THREADS;
-                    if (c < chunks) {
-                        load8(xb, w0, chunk_off(c), in_lo, in_hi, v[i]);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) v[i][k] = 0.0f;
-                    }
-                }
-                // chunks beyond the register share: max only (re-read after the wait)
-                for (int c = ct + CONV_RC * UM_CONV_THREADS; c < chunks; c += UM_CONV_THREADS) {
-                    float t[8];
-                    load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(t[k]));
-                }
-#pragma unroll
-                for (int i = 0; i < CONV_RC; ++i)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(v[i][k]));
 #pragma unroll
                 for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
                 if (lane == 0) red[cw] = mx;
@@ -1144,6 +1154,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
+                if (warp == 2 + UM_CONV_WARPS && p == A.n_passes - 1) WH_TRACE(10, ucnt);
                 if (lane == 0) {
                     // TMEM accesses are ordered by wait::st + fence::before_thread_sync; the
                     // global stores need no ordering against the MMA: relaxed arrive
@@ -1345,6 +1356,10 @@ int umma_prepare(Plan &p) {
         H = 256;
     }
     p.V = (int32_t)(H <= 64 ? 64 : H);
+    if (const char *v = std::getenv("WH_UMMA_V")) {  // experiment: more phases per row
+        const int vv = std::atoi(v);
+        if (vv >= p.V && vv % 64 == 0 && vv % H == 0 && p.rs == 1) p.V = vv;
+    }
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
     p.panels = p.V / 64;
@@ -1568,8 +1583,8 @@ int umma_prepare(Plan &p) {
     p.res_bytes = res_bytes;
     p.n_stream = n_stream;
     const int64_t stage_bytes = std::max<int64_t>(max_group, 1024);
-    const int64_t table_bytes = 16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
-                                16 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S;
+    const int64_t table_bytes = (16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
+                                 16 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S + 15) / 16 * 16;
     // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
     // alignment slack and the tables
     UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
@@ -1640,6 +1655,46 @@ int umma_prepare(Plan &p) {
     p.ring_bytes = ring;
     p.smem_bytes = (size_t)((win_bufs + use_stg) * win + ring) + 1024 + table_bytes;
 
+    {
+        // the kernel's shared-memory tables, packed here in their smem layout so that one
+        // bulk copy loads them at launch: int4 pass[], int4 group[], uint4 tile[] (pre-decoded
+        // MMA operands of each K-step, in 16-byte descriptor units: x = A offset in the window
+        // | c0 << 16, y = B offset in the group | MMA2's B delta << 16, z / w = instruction
+        // descriptors of MMA1 (N = nc + ncorr) / MMA2 (N = ncorr; 0 = not issued)), int goff[]
+        // (resident groups' smem offsets), float spow[] (per-scale 2^-f)
+        std::vector<uint8_t> blob((size_t)table_bytes, 0);
+        uint8_t *w = blob.data();
+        auto put32 = [&](uint32_t v) { std::memcpy(w, &v, 4); w += 4; };
+        for (auto &ps : p.passes) {
+            put32((uint32_t)ps.group_begin); put32((uint32_t)ps.group_end);
+            put32((uint32_t)ps.s0 | ((uint32_t)ps.ns << 16)); put32((uint32_t)ps.cols);
+        }
+        for (auto &g : p.groups_u) {
+            put32((uint32_t)g.tile_begin); put32((uint32_t)g.tile_end);
+            put32((uint32_t)(g.bank_off >> 7)); put32((uint32_t)g.cta_bytes);
+        }
+        auto idesc = [&](uint32_t n) { return (1u << 4) | ((n >> 3) << 17) | (((128u * (uint32_t)p.cg) >> 4) << 24); };
+        for (auto &tl : p.tiles) {
+            // window row shift q and panel of this K-step's A operand (k*64 = q*V + panel*64)
+            const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)p.V, panel = (kg % (uint32_t)p.V) >> 6;
+            const uint32_t aoff = panel * (uint32_t)p.win_rows * 128u + q * 128u;
+            const uint32_t n1 = (uint32_t)(tl.ncols + tl.ncorr), n2 = (uint32_t)tl.ncorr;
+            const uint32_t b2d = (p.cg == 2 ? n1 / 2 : n1) * 128u;
+            put32((aoff >> 4) | ((uint32_t)tl.c0 << 16));
+            put32(((uint32_t)tl.in_off >> 4) | ((b2d >> 4) << 16));
+            put32(idesc(n1));
+            put32(n2 ? idesc(n2) : 0u);
+        }
+        for (auto &g : p.groups_u) put32((uint32_t)g.pad_);
+        for (int i = 0; i < p.S; ++i) {
+            uint32_t v;
+            std::memcpy(&v, &spow[i], 4);
+            put32(v);
+        }
+        p.tables_bytes = table_bytes;
+        WH_CUDA_TRY(cudaMalloc(&p.d_tables, (size_t)table_bytes));
+        WH_CUDA_TRY(cudaMemcpy(p.d_tables, blob.data(), (size_t)table_bytes, cudaMemcpyHostToDevice));
+    }
     WH_CUDA_TRY(cudaMalloc(&p.d_passes, sizeof(UmmaPass) * p.passes.size()));
     WH_CUDA_TRY(cudaMalloc(&p.d_tiles, sizeof(UmmaTile) * p.tiles.size()));
     WH_CUDA_TRY(cudaMalloc(&p.d_groups_u, sizeof(UmmaGroup) * p.groups_u.size()));
@@ -1714,6 +1769,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.cpr_shift = p.panels == 1 ? 3 : p.panels == 2 ? 4 : p.panels == 4 ? 5 : -1;
     a.conv_regs = (!p.use_stg && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
+    a.tables = p.d_tables; a.tables_bytes = (uint32_t)p.tables_bytes;
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
     a.minmax = p.norm != WH_NORM_NONE ? mm : nullptr;
