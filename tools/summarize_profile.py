@@ -35,7 +35,11 @@ for k, (n, v) in agg.items():
     lines.append(f'"{k}",{n},{v:.0f},{v / tot:.3f}')
 open(f"{out}/{tag}_launches_summary.csv", "w").write("\n".join(lines) + "\n")
 shutil.copy(f"gpurun_out/launches_{tag}.csv", f"{out}/{tag}_launches.csv")
-shutil.copy(f"gpurun_out/bench_{tag}.json", f"{out}/{tag}_bench_c2.json")
+for c in ("c2", "c5", "ref"):
+    if os.path.exists(f"gpurun_out/bench_{c}_{tag}.json"):
+        shutil.copy(f"gpurun_out/bench_{c}_{tag}.json", f"{out}/{tag}_bench_{c}.json")
+if os.path.exists(f"gpurun_out/bench_{tag}.json"):
+    shutil.copy(f"gpurun_out/bench_{tag}.json", f"{out}/{tag}_bench_c2.json")
 # full capture -> key metrics
 rep = f"gpurun_out/prof_umma_c2_{tag}.ncu-rep"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
