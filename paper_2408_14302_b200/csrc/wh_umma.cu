@@ -77,7 +77,7 @@ struct UmmaArgs {
     unsigned long long *prof;       // optional per-role wait counters (wh_plan_profile)
     int32_t dbg;                    // diagnostics (WH_UMMA_DBG bits, results invalid): 1 no epilogue work,
                                     // 2 no converter work, 4 no MMA, 8 cluster-scope window release,
-                                    // 32 no output stores, 64 no accumulator re-zeroing,
+                                    // 32 no output values or stores, 64 no accumulator re-zeroing, 2048 no store instructions,
                                     // 128 no streamed tap copies after the first unit
     long long *trace;               // diagnostics: CTA-0 timeline [event][unit] (WH_UMMA_TRACE)
 };
@@ -389,16 +389,28 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                 // per-lane scalar (8-byte) stores, which compete with the UMMA operand reads
                 // for the SM's data path.
                 const int li = lane_id();
+                // per-scale factors of the SPU scales of this unit (s0 + sl0 is a multiple of
+                // 4 and s_spow 16-byte aligned): SPU/4 vector loads; scales >= ns contribute 0
+                float f[SPU];
+#pragma unroll
+                for (int q = 0; q < SPU; q += 4) {
+                    const float4 sp = *reinterpret_cast<const float4 *>(spow + s0 + sl0 + q);
+                    f[q] = e * sp.x; f[q + 1] = e * sp.y; f[q + 2] = e * sp.z; f[q + 3] = e * sp.w;
+                }
+                if (sl0 + SPU > ns) {
+#pragma unroll
+                    for (int q = 0; q < SPU; ++q)
+                        if (sl0 + q >= ns) f[q] = 0.0f;
+                }
                 float val[SPU][P];
 #pragma unroll
                 for (int q = 0; q < SPU; ++q) {
-                    const float f = (sl0 + q < ns) ? e * spow[s0 + sl0 + q] : 0.0f;
 #pragma unroll
                     for (int r = 0; r < P; ++r) {
-                        const float x = (v[q * CP + r] + wr[15 - (q * CP + r)]) * f;
+                        const float x = (v[q * CP + r] + wr[15 - (q * CP + r)]) * f[q];
                         float mag;
                         if constexpr (CC == 2) {
-                            const float y = (v[q * CP + P + r] + wr[15 - (q * CP + P + r)]) * f;
+                            const float y = (v[q * CP + P + r] + wr[15 - (q * CP + P + r)]) * f[q];
                             mag = sqrtf(fmaf(x, x, y * y));
                         } else {
                             mag = fabsf(x);
@@ -420,8 +432,13 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                 const int gi = li & (LPG - 1);
                 const int64_t fq = frame0 - (int64_t)gi * P;  // first frame of the lane group
                 const int nq = (int)(F - fq < 4 ? (F - fq > 0 ? F - fq : 0) : 4);
+                const bool st4 = nq == 4 && vec;
+                // this lane's scale for store group g is sl0 + LPG*g + gi: one row pointer,
+                // advanced by LPG rows per group
+                float *dst = reinterpret_cast<float *>(A.out) + (b * A.S + s0 + sl0 + gi) * F + fq;
+                const int64_t gstep = (int64_t)LPG * F;
 #pragma unroll
-                for (int g = 0; g < SPU / LPG; ++g) {
+                for (int g = 0; g < SPU / LPG; ++g, dst += gstep) {
                     float t[4];
                     if constexpr (P == 1) {
 #pragma unroll
@@ -456,11 +473,10 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                             }
                         }
                     }
-                    // this lane now holds scale sl0 + LPG*g + gi for frames fq .. fq + 3
-                    const int sc = sl0 + LPG * g + gi;
-                    if (sc < ns && nq > 0) {
-                        float *dst = reinterpret_cast<float *>(A.out) + (b * A.S + s0 + sc) * F + fq;
-                        if (nq == 4 && vec) {
+                    if (A.dbg & 2048) {  // diagnostics: everything but the store instruction
+                        if (t[0] + t[1] + t[2] + t[3] == 12345.678f) lmin = 0.0f;
+                    } else if (sl0 + LPG * g + gi < ns) {
+                        if (st4) {
                             st_na(reinterpret_cast<float4 *>(dst), make_float4(t[0], t[1], t[2], t[3]));
                         } else {
 #pragma unroll
@@ -624,8 +640,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                                             (A.use_stg ? 2 * (size_t)WH : 0));
     int4 *s_group = s_pass + A.n_passes;
     uint4 *s_tile = reinterpret_cast<uint4 *>(s_group + A.n_groups);
-    int *s_goff = reinterpret_cast<int *>(s_tile + A.n_tiles);  // resident: smem offset per group
-    float *s_spow = reinterpret_cast<float *>(s_goff + A.n_groups);
+    float *s_spow = reinterpret_cast<float *>(s_tile + A.n_tiles);  // per-scale 2^-f (16-byte aligned)
+    int *s_goff = reinterpret_cast<int *>(s_spow + ((A.S + 15) & ~15));  // resident: smem offset per group
     // the tables arrive by one bulk copy (one HBM round trip at launch; the host packed them
     // in their smem layout)
     if (threadIdx.x == 0) {
@@ -1339,7 +1355,7 @@ static int ncheck_tiles(const Plan &p) {
     for (auto &t : p.tiles)
         if ((int64_t)t.k * 64 / p.V >= 4096 || p.V / 64 > 16 || t.c0 > 255 || t.ncols > 255 || (t.byte_off & 127))
             return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table out of range");
-    if (16 * p.passes.size() + 20 * p.groups_u.size() + 16 * p.tiles.size() + 4 * (size_t)p.S > 32 * 1024)
+    if (16 * p.passes.size() + 20 * p.groups_u.size() + 16 * p.tiles.size() + 4 * (size_t)((p.S + 15) / 16 * 16) > 32 * 1024)
         return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table too large");
     return WH_OK;
 }
@@ -1584,7 +1600,7 @@ int umma_prepare(Plan &p) {
     p.n_stream = n_stream;
     const int64_t stage_bytes = std::max<int64_t>(max_group, 1024);
     const int64_t table_bytes = (16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
-                                 16 * (int64_t)p.tiles.size() + 4 * (int64_t)p.S + 15) / 16 * 16;
+                                 16 * (int64_t)p.tiles.size() + 4 * (int64_t)((p.S + 15) / 16 * 16) + 15) / 16 * 16;
     // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
     // alignment slack and the tables
     UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
@@ -1660,8 +1676,8 @@ int umma_prepare(Plan &p) {
         // bulk copy loads them at launch: int4 pass[], int4 group[], uint4 tile[] (pre-decoded
         // MMA operands of each K-step, in 16-byte descriptor units: x = A offset in the window
         // | c0 << 16, y = B offset in the group | MMA2's B delta << 16, z / w = instruction
-        // descriptors of MMA1 (N = nc + ncorr) / MMA2 (N = ncorr; 0 = not issued)), int goff[]
-        // (resident groups' smem offsets), float spow[] (per-scale 2^-f)
+        // descriptors of MMA1 (N = nc + ncorr) / MMA2 (N = ncorr; 0 = not issued)), float spow[]
+        // (per-scale 2^-f, padded to 16: the epilogue reads whole 16-column units), int goff[] (resident groups' smem offsets)
         std::vector<uint8_t> blob((size_t)table_bytes, 0);
         uint8_t *w = blob.data();
         auto put32 = [&](uint32_t v) { std::memcpy(w, &v, 4); w += 4; };
@@ -1685,12 +1701,12 @@ int umma_prepare(Plan &p) {
             put32(idesc(n1));
             put32(n2 ? idesc(n2) : 0u);
         }
-        for (auto &g : p.groups_u) put32((uint32_t)g.pad_);
-        for (int i = 0; i < p.S; ++i) {
-            uint32_t v;
-            std::memcpy(&v, &spow[i], 4);
+        for (int i = 0; i < (p.S + 15) / 16 * 16; ++i) {
+            uint32_t v = 0;
+            if (i < p.S) std::memcpy(&v, &spow[i], 4);
             put32(v);
         }
+        for (auto &g : p.groups_u) put32((uint32_t)g.pad_);
         p.tables_bytes = table_bytes;
         WH_CUDA_TRY(cudaMalloc(&p.d_tables, (size_t)table_bytes));
         WH_CUDA_TRY(cudaMemcpy(p.d_tables, blob.data(), (size_t)table_bytes, cudaMemcpyHostToDevice));
