@@ -108,6 +108,7 @@ struct Plan {
     float *d_scale_pow = nullptr;  // per scale 2^-f_s
     uint8_t *d_tables = nullptr;   // UMMA: the kernel's smem tables, packed (one bulk copy)
     int64_t tables_bytes = 0;
+    double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
     std::vector<int32_t> fexp;
     int32_t bstages = 2, win_bufs = 2;     // bstages: full-width tiles the ring holds (info)
     int64_t ring_bytes = 0;                // tap-tile ring capacity

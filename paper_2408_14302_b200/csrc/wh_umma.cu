@@ -55,6 +55,7 @@ struct UmmaArgs {
     int32_t row_tiles, V, P, Cc, panels, G0, win_rows, S;
     int32_t rs;                         // rows per frame (hop = 256 * rs > 256), else 1
     int32_t n_passes, n_tiles, wavelet, output, win_bufs, vec_ok;
+    int32_t pgroups, ppu;               // a unit = (clip, tile pair, group of ppu passes); pgroups groups
     int32_t n_acc, acc_stride;          // accumulator buffers; columns per buffer (main|corr)
     int32_t use_stg;                    // fp32 window staged in smem by cp.async.bulk
     int32_t resident;                   // some tap groups live in smem for the whole kernel
@@ -570,10 +571,17 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     const int64_t u0 = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
     const int64_t ustride = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
     const int64_t tpu = (A.row_tiles + CG - 1) / CG;
-    const int64_t n_units = A.clips * tpu;
+    const int64_t n_units = A.clips * tpu * A.pgroups;
+    // unit u: pass group u % pgroups of tile pair (u / pgroups) -- consecutive units (the pass
+    // groups of one tile pair) go to different CTA pairs
     auto unit_tile = [&](int64_t u, int64_t &b, int64_t &tile) {
-        b = u / tpu;
-        tile = CG * (u % tpu) + rank;
+        const int64_t v = u / A.pgroups;
+        b = v / tpu;
+        tile = CG * (v % tpu) + rank;
+    };
+    auto unit_passes = [&](int64_t u, int &p0, int &p1) {
+        p0 = (int)(u % A.pgroups) * A.ppu;
+        p1 = p0 + A.ppu < A.n_passes ? p0 + A.ppu : A.n_passes;
     };
     // Converters, register-prefetch path: each thread loads its first CONV_RC 8-sample chunks
     // of a unit's window into registers (cv) and the window's max |x| over all its chunks
@@ -726,7 +734,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         uint32_t seq = 0, tail = 0;
         const uint32_t RING = A.ring_bytes - A.res_bytes;
         for (int64_t item = A.n_stream ? u0 : n_units; item < n_units; item += ustride) {
-            for (int p = 0; p < A.n_passes; ++p) {
+            int pb, pe;
+            unit_passes(item, pb, pe);
+            for (int p = pb; p < pe; ++p) {
                 const int4 pinfo = s_pass[p];
                 for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
                     if (s_goff[gi] >= 0) continue;  // resident
@@ -779,7 +789,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             tc_fence_after();
             WH_TRACE(1, wcnt);
             const uint32_t a_hi16 = (smem_u32(win_base) + wb * 2 * WH) >> 4, wh16 = WH >> 4;
-            for (int p = 0; p < A.n_passes; ++p, ++acnt) {
+            int pb, pe;
+            unit_passes(item, pb, pe);
+            for (int p = pb; p < pe; ++p, ++acnt) {
                 const int4 pinfo = s_pass[p];
                 const uint32_t ab = acnt % A.n_acc;
                 mbar_wait_p(&acc_empty[ab], ((acnt / A.n_acc) & 1) ^ 1, pa, 1, pon);
@@ -852,7 +864,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             __syncwarp();
         }
         for (int64_t item = A.n_stream ? u0 : n_units; item < n_units; item += ustride) {
-            for (int p = 0; p < A.n_passes; ++p) {
+            int pb, pe;
+            unit_passes(item, pb, pe);
+            for (int p = pb; p < pe; ++p) {
                 const int4 pinfo = s_pass[p];
                 for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
                     if (s_goff[gi] >= 0) continue;
@@ -1136,13 +1150,15 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 lmax = -INFINITY;
                 cur_b = b;
             }
-            for (int p = 0; p < A.n_passes; ++p, ++acnt) {
+            int pb, pe;
+            unit_passes(item, pb, pe);
+            for (int p = pb; p < pe; ++p, ++acnt) {
                 const int4 pinfo = s_pass[p];
                 const uint32_t ab = acnt % A.n_acc;
-                if (warp == 2 + UM_CONV_WARPS && p == 0) WH_TRACE(8, ucnt);
+                if (warp == 2 + UM_CONV_WARPS && p == pb) WH_TRACE(8, ucnt);
                 mbar_wait_p(&acc_full[ab], (acnt / A.n_acc) & 1, pa, 0, pon);
                 tc_fence_after();
-                if (warp == 2 + UM_CONV_WARPS && p == 0) WH_TRACE(9, ucnt);
+                if (warp == 2 + UM_CONV_WARPS && p == pb) WH_TRACE(9, ucnt);
                 const float e = xring[ucnt & 3];
                 const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + ab * (uint32_t)A.acc_stride;
                 // corr_j lives at column 2C-1-j: the 16 corr values of unit u0 are loaded
@@ -1170,7 +1186,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
                 __syncwarp();
-                if (warp == 2 + UM_CONV_WARPS && p == A.n_passes - 1) WH_TRACE(10, ucnt);
+                if (warp == 2 + UM_CONV_WARPS && p == pe - 1) WH_TRACE(10, ucnt);
                 if (lane == 0) {
                     // TMEM accesses are ordered by wait::st + fence::before_thread_sync; the
                     // global stores need no ordering against the MMA: relaxed arrive
@@ -1494,7 +1510,7 @@ int umma_prepare(Plan &p) {
         }
         p.G0 = (int32_t)best;
     }
-    make_tiles(p.G0, p.passes, p.tiles);
+    p.unit_cost = make_tiles(p.G0, p.passes, p.tiles);
     p.Qlo = (int32_t)((p.G0 + p.V - 1) / p.V);
     p.ksteps = (int32_t)((p.G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1);
     const int64_t qmax = (int64_t)(p.ksteps - 1) * 64 / p.V;
@@ -1796,7 +1812,29 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.prof = p.d_prof;
     a.dbg = std::getenv("WH_UMMA_DBG") ? std::atoi(std::getenv("WH_UMMA_DBG")) : 0;
     a.trace = p.d_trace;
-    const int64_t units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
+    // Split each tile pair's passes into G groups (separate units) when there are too few
+    // units to fill the CTA pairs evenly (c3: 80 tile pairs on 74 CTA pairs): minimise
+    // rounds x unit time, with a unit costing at least one window conversion (~6 k cycles)
+    const int64_t tile_units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
+    const int64_t pairs = std::max<int64_t>(1, p.grid_ctas / p.cg);
+    const int n_passes = (int)p.passes.size();
+    int G = 1;
+    double best = -1.0;
+    for (int g = 1; g <= n_passes; ++g) {
+        const int ppu = (n_passes + g - 1) / g;
+        const int gg = (n_passes + ppu - 1) / ppu;  // groups actually formed
+        if (gg != g) continue;
+        const double rounds = std::ceil((double)(tile_units * g) / (double)pairs);
+        const double t = rounds * std::max(p.unit_cost * (double)ppu / n_passes, 6000.0);
+        if (best < 0 || t < best * 0.97) {
+            best = t;
+            G = g;
+        }
+    }
+    if (const char *e = std::getenv("WH_UMMA_PGROUPS")) G = std::max(1, std::min(n_passes, std::atoi(e)));
+    a.ppu = (n_passes + G - 1) / G;
+    a.pgroups = (n_passes + a.ppu - 1) / a.ppu;
+    const int64_t units = tile_units * a.pgroups;
     int64_t grid = std::min<int64_t>(units * p.cg, p.grid_ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls

@@ -335,6 +335,26 @@ def test_umma_planner_variants_agree(env, monkeypatch):
             assert row_rel_err(got, ref) <= ROW_TOL, env
 
 
+@pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
+def test_pass_groups_are_byte_identical(groups, monkeypatch):
+    """Splitting a tile pair's passes into separate units (what the launcher does when there
+    are fewer tile pairs than CTA pairs, e.g. c3) changes only which CTA computes a pass:
+    the outputs are byte-identical to the unsplit launch (hop 1: 32 passes; c5-like cmor
+    min-max: 5 passes, the per-clip min / max then combines partial units)."""
+    for cid, hop, wavelet, output, norm, clips, n in ((3, 1, "rmor", "abs", None, 2, 20000),
+                                                      (5, 32, "cmor", "abs", "minmax", 3, 40000)):
+        x = synth.make_batch(cid, clips=clips, n=n, start=1)
+        sc = synth.config_scales(cid)
+        plan = wh.CwthPlan(sc, None, hop, n, wavelet=wavelet, output=output, norm=norm,
+                           max_clips=clips, engine="umma")
+        monkeypatch.setenv("WH_UMMA_PGROUPS", "1")
+        one = plan.execute_host(x).copy()
+        monkeypatch.setenv("WH_UMMA_PGROUPS", groups)
+        split = plan.execute_host(x)
+        plan.close()
+        assert one.tobytes() == split.tobytes(), (cid, groups)
+
+
 @pytest.mark.parametrize("engine", ["umma", "simt"])
 def test_unaligned_rows_and_odd_lengths(engine):
     """ld_x not a multiple of 4 (no 16-byte vector loads) and N not a multiple of the hop:
