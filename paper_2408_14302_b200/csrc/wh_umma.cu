@@ -75,6 +75,7 @@ struct UmmaArgs {
     uint32_t *minmax;
     uint32_t ring_bytes, win_half_bytes;
     int32_t out_vec_ok;             // output base 16B aligned and F % 4 == 0
+    int32_t out_vec8_ok;            // output base 32B aligned and F % 8 == 0 (256-bit stores)
     unsigned long long *prof;       // optional per-role wait counters (wh_plan_profile)
     int32_t dbg;                    // diagnostics (WH_UMMA_DBG bits, results invalid): 1 no epilogue work,
                                     // 2 no converter work, 4 no MMA, 8 cluster-scope window release,
@@ -283,6 +284,30 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t ta, uint32_t tb, float (&va
     }
 }
 
+// two 32-column TMEM loads (this warp's 32 lanes) and one wait: main columns [ta, ta+32) and
+// the matching correction columns [tb, tb+32)
+__device__ __forceinline__ void tmem_ld32x2(uint32_t ta, uint32_t tb, float (&va)[32], float (&vb)[32]) {
+    uint32_t r[32], q[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+          "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]), "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]), "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
+        : "r"(ta), "r"(tb)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        va[i] = __uint_as_float(r[i]);
+        vb[i] = __uint_as_float(q[i]);
+    }
+}
+__device__ __forceinline__ void tmem_st32_zero(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u)
+        : "memory");
+}
+
 __device__ __forceinline__ float lg2_fast(float x) {
     float y;
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -310,6 +335,12 @@ __device__ __forceinline__ void st_na(float2 *p, float2 v) {
 __device__ __forceinline__ void st_na(float4 *p, float4 v) {
     asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                  "f"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_na8(float *p, const float *v) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                  : "memory");
 }
 
@@ -344,7 +375,12 @@ __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nval
                 }
         }
         float *dst = reinterpret_cast<float *>(A.out) + o;
-        if (R % 4 == 0 && nvalid == R && vec) {
+        if (R % 8 == 0 && nvalid == R && vec && A.out_vec8_ok) {
+            // 32 bytes per lane: whole sectors, half the store transactions of 16-byte stores
+            // (lanes of a warp hold different rows: every lane's piece is its own transaction)
+#pragma unroll
+            for (int r = 0; r < R; r += 8) st_na8(dst + r, val + (r % R));
+        } else if (R % 4 == 0 && nvalid == R && vec) {
 #pragma unroll
             for (int r = 0; r < R; r += 4)
                 st_na(reinterpret_cast<float4 *>(dst + r),
@@ -510,6 +546,81 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
         }
     } else {
         // P >= 16: per scale, 16-phase chunks of re (and im); the two warps take alternate scales
+        if constexpr (CC == 1 && P % 32 == 0 && OUT != WH_OUT_COMPLEX64) if (vec && A.out_vec8_ok) {
+            // Real outputs, P = 32 / 64 (hop 2 / 1): a lane holds 32 consecutive frames of
+            // its row; a 4 x 4 transpose of 8-frame blocks inside each lane quad gives every
+            // lane 8 frames of each of the quad's 4 rows, so one 32-byte store per lane writes
+            // whole 128-byte lines (4 lanes per line): a quarter of the store transactions of
+            // per-row stores, which bound the hop-1 epilogue.
+            const int gi = lane_id() & 3;
+            const int64_t qf0 = frame0 - (int64_t)gi * P;  // first frame of the quad's first row
+            for (int sl = half; sl < ns; sl += 2) {
+                const float f = e * spow[s0 + sl];
+                float *rowbase = reinterpret_cast<float *>(A.out) + (b * A.S + s0 + sl) * F;
+#pragma unroll 1
+                for (int r0 = 0; r0 < P; r0 += 32) {
+                    float t[4][8];
+                    {
+                        // main columns u0 .. u0+31 and their correction columns (stored reversed
+                        // at 2C-1-j: one 32-column range ending at cbase + 16 - u0)
+                        const uint32_t u0 = (uint32_t)(sl * CP + r0);
+                        float re[32], w[32];
+                        tmem_ld32x2(tbase + u0, cbase - 16u - u0, re, w);
+                        tmem_st32_zero(tbase + u0);
+                        tmem_st32_zero(cbase - 16u - u0);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) t[i / 8][i % 8] = out_value<OUT>(fabsf((re[i] + w[31 - i]) * f));
+                    }
+                    if (A.minmax) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                if (r0 + 8 * k + i < nvalid) {
+                                    lmin = fminf(lmin, t[k][i]);
+                                    lmax = fmaxf(lmax, t[k][i]);
+                                }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 2; ++k)  // exchange the off-diagonal 2 x 2 block quadrants
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float v = (gi & 2) ? t[k][i] : t[2 + k][i];
+                            const float x = __shfl_xor_sync(0xffffffffu, v, 2);
+                            if (gi & 2) t[k][i] = x;
+                            else t[2 + k][i] = x;
+                        }
+#pragma unroll
+                    for (int k = 0; k < 4; k += 2)  // transpose the 2 x 2 blocks
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float v = (gi & 1) ? t[k][i] : t[k + 1][i];
+                            const float x = __shfl_xor_sync(0xffffffffu, v, 1);
+                            if (gi & 1) t[k][i] = x;
+                            else t[k + 1][i] = x;
+                        }
+                    // t[j] = frames r0 + 8 gi .. + 7 of the quad's row j
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int64_t fr = qf0 + (int64_t)j * P + r0 + 8 * gi;
+                        float *dst = rowbase + fr;
+                        if (F - fr >= 8) {
+                            st_na8(dst, t[j]);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                if (i < F - fr) st_na(dst + i, t[j][i]);
+                        }
+                    }
+                }
+            }
+            if (half == 0)
+                for (int c = ns * CP; c < cols; c += 16) {
+                    tmem_st16_zero(tbase + c);
+                    tmem_st16_zero(cbase - c);
+                }
+            return;
+        }
         for (int sl = half; sl < ns; sl += 2) {
             const float f = e * spow[s0 + sl];
 #pragma unroll 1
@@ -1809,6 +1920,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.ring_bytes = (uint32_t)p.ring_bytes;
     a.win_half_bytes = (uint32_t)p.panels * (uint32_t)p.win_rows * 128u;
     a.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (p.F % 4 == 0);
+    a.out_vec8_ok = ((reinterpret_cast<uintptr_t>(out) & 31) == 0) && (p.F % 8 == 0);
     a.prof = p.d_prof;
     a.dbg = std::getenv("WH_UMMA_DBG") ? std::atoi(std::getenv("WH_UMMA_DBG")) : 0;
     a.trace = p.d_trace;
