@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -438,7 +439,9 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
     // chunk j+1, the kernel of chunk j and the D2H copy of chunk j-1 overlap (PCIe is full
     // duplex).  Pageable buffers: one chunk (the copies are staged by the driver anyway).
     const bool pinned = is_pinned(x_host) && is_pinned(out_host);
-    const int64_t n_chunks = (pinned && clips >= 4) ? std::min<int64_t>(8, clips) : 1;
+    int64_t max_chunks = 8;
+    if (const char *c = std::getenv("WH_HOST_CHUNKS")) max_chunks = std::max(1, std::atoi(c));  // experiments
+    const int64_t n_chunks = (pinned && clips >= 4) ? std::min<int64_t>(max_chunks, clips) : 1;
     const int64_t per = (clips + n_chunks - 1) / n_chunks;
     const size_t out_clip = (size_t)p->S * p->F * out_elem_bytes(*p);
     int rc = WH_OK;
