@@ -32,6 +32,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -61,7 +62,7 @@ struct UmmaArgs {
     int32_t resident;                   // some tap groups live in smem for the whole kernel
     uint32_t res_bytes;                 // bytes of the resident region at the stage base
     int32_t n_stream;                   // tap groups streamed through the ring every unit
-    int32_t cpr_shift;                  // log2(8-sample chunks per window row) = log2(panels * 8)
+    int32_t cpr, cpr_magic;             // 8-sample chunks per window row (panels * 8); ceil(2^20 / cpr)
     int32_t conv_regs;                  // converters prefetch the window into registers
     const UmmaPass *passes;
     const UmmaTile *tiles;
@@ -655,6 +656,14 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
     }
 }
 
+// window chunk c (8 consecutive samples) -> (row, chunk within the row) for cpr = panels * 8
+// chunks per row: row = (c * ceil(2^20 / cpr)) >> 20, exact for c < 131 k when cpr = 24 (checked
+// exhaustively; windows have < 5 k chunks), and for any c when cpr is a power of two
+__device__ __forceinline__ void chunk_rc(const UmmaArgs &A, int c, int &row, int &cc) {
+    row = (int)(((uint32_t)c * (uint32_t)A.cpr_magic) >> 20);
+    cc = c - row * A.cpr;
+}
+
 // ---- the kernel --------------------------------------------------------------------------
 template <int CC, int P, int CG>
 __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ UmmaArgs A) {
@@ -723,8 +732,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const int64_t in_hi64 = A.N - w0;
         const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
         const int ct = (int)threadIdx.x - 64, chunks = A.win_rows * A.panels * 8;
-        const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
-        auto chunk_off = [&](int c) { return (int32_t)((c >> cpr_shift) * A.V + (c & cpr_mask) * 8); };
+        auto chunk_off = [&](int c) {
+            int row, cc;
+            chunk_rc(A, c, row, cc);
+            return (int32_t)(row * A.V + cc * 8);
+        };
 #pragma unroll
         for (int i = 0; i < CONV_RC; ++i) {
             const int c = ct + i * UM_CONV_THREADS;
@@ -1033,7 +1045,6 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             // run, then converts from registers once the window buffer is free.  Larger
             // windows (c5: 13.5 chunks per thread) read their extra chunks twice: once
             // before the wait for the window max, again (L2 hits) after it.
-            const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
             auto load8 = conv_load8;
             auto split8 = [&](const float (&in)[8], float sc, uint32_t (&hw)[4], uint32_t (&lw)[4]) {
 #pragma unroll
@@ -1061,7 +1072,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 if (item != u0) conv_fetch(item);
                 float (&v)[CONV_RC][8] = cv;
                 float mx = cmx;
-                auto chunk_off = [&](int c) { return (int32_t)((c >> cpr_shift) * A.V + (c & cpr_mask) * 8); };
+                auto chunk_off = [&](int c) {
+            int row, cc;
+            chunk_rc(A, c, row, cc);
+            return (int32_t)(row * A.V + cc * 8);
+        };
 #pragma unroll
                 for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
                 if (lane == 0) red[cw] = mx;
@@ -1093,7 +1108,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 uint8_t *whi = win_base + (size_t)wb * 2 * WH;
                 uint8_t *wlo = whi + WH;
                 auto put = [&](int c, const uint32_t (&hw)[4], const uint32_t (&lw)[4]) {
-                    const int row = c >> cpr_shift, cc = c & cpr_mask;
+                    int row, cc;
+                    chunk_rc(A, c, row, cc);
                     const int panel = cc >> 3, c8 = cc & 7;
                     const uint32_t off =
                         (uint32_t)panel * panel_bytes + (uint32_t)row * 128u + (uint32_t)((c8 ^ (row & 7)) * 16);
@@ -1140,9 +1156,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             if (ct == 0) WH_TRACE(3, wcnt);
             if (A.use_stg) mbar_wait_p(&stg_full, wcnt & 1, pa, 0, pon);
             if (ct == 0) WH_TRACE(4, wcnt);
-            // chunk c = 8 consecutive samples: row = c >> cpr_shift, column chunk = c & cpr_mask
-            // (cpr = panels * 8 chunks per row); window offsets are 32-bit
-            const int cpr_shift = A.cpr_shift, cpr_mask = (1 << cpr_shift) - 1;
+            // chunk c = 8 consecutive samples: (row, column chunk) = chunk_rc(c) (cpr = panels * 8
+            // chunks per row); window offsets are 32-bit
             const int32_t st_lo = (int32_t)(slo - w0), st_hi = (int32_t)(shi - w0);  // staged range
             const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);                       // clip start
             const int64_t in_hi64 = A.N - w0;                                          // clip end
@@ -1165,7 +1180,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 }
             };
             auto chunk_off = [&](int c) {
-                const int row = c >> cpr_shift, cc = c & cpr_mask;  // cc = panel * 8 + c8
+                int row, cc;  // cc = panel * 8 + c8
+                chunk_rc(A, c, row, cc);
                 return row * A.V + cc * 8;
             };
             // pass 1: max |x| over the window
@@ -1198,7 +1214,8 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             uint8_t *wlo = whi + WH;
 #pragma unroll 2
             for (int c = ct; c < ((A.dbg & 2) ? 0 : chunks); c += UM_CONV_THREADS) {
-                const int row = c >> cpr_shift, cc = c & cpr_mask;
+                int row, cc;
+                    chunk_rc(A, c, row, cc);
                 const int panel = cc >> 3, c8 = cc & 7;
                 float v[8];
                 load8(row * A.V + cc * 8, v);
@@ -1452,11 +1469,13 @@ int umma_supported(const Plan &p, std::string *why) {
     const bool small = H <= 64 && 64 % H == 0;
     const bool big = H % 64 == 0 && H <= 256;
     const bool strided = H > 256 && H % 256 == 0;  // rows of 256 samples, every (H/256)-th a frame
-    if (!small && !big && !strided) {
-        if (why) *why = "hop must divide 64, or be a multiple of 64 up to 256, or a multiple of 256";
+    const int64_t lcm64 = H / std::gcd(H, (int64_t)64) * 64;
+    const bool mid = !small && !big && !strided && lcm64 <= 256;  // 3, 6, 12, 24, 48, 96: rows of 192
+    if (!small && !big && !strided && !mid) {
+        if (why) *why = "hop must divide 64 or 192, or be a multiple of 64 up to 256, or a multiple of 256";
         return WH_E_UNSUPPORTED;
     }
-    const int64_t V = small ? 64 : (big ? H : 256);
+    const int64_t V = small ? 64 : (big ? H : (mid ? lcm64 : 256));
     const int64_t P = strided ? 1 : V / H;
     const int64_t maxg = (p.Lmax + V - 1) / V * V + p.Lmax + (P - 1) * (strided ? 0 : H);  // longest K range
     const int64_t ksteps = maxg / 64 + 1;
@@ -1498,7 +1517,9 @@ int umma_prepare(Plan &p) {
         p.rs = (int32_t)(H / 256);
         H = 256;
     }
-    p.V = (int32_t)(H <= 64 ? 64 : H);
+    // rows of V = lcm(hop, 64) samples (<= 256): hop | 64 -> 64, hop | 192 -> 192, hop = 128,
+    // 192, 256 -> hop; P = V / hop frames (phases) per row
+    p.V = (int32_t)(H / std::gcd(H, (int64_t)64) * 64);
     if (const char *v = std::getenv("WH_UMMA_V")) {  // experiment: more phases per row
         const int vv = std::atoi(v);
         if (vv >= p.V && vv % 64 == 0 && vv % H == 0 && p.rs == 1) p.V = vv;
@@ -1909,7 +1930,8 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.resident = p.resident;
     a.res_bytes = (uint32_t)p.res_bytes;
     a.n_stream = p.n_stream;
-    a.cpr_shift = p.panels == 1 ? 3 : p.panels == 2 ? 4 : p.panels == 4 ? 5 : -1;
+    a.cpr = p.panels * 8;
+    a.cpr_magic = ((1 << 20) + a.cpr - 1) / a.cpr;
     a.conv_regs = (!p.use_stg && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.tables = p.d_tables; a.tables_bytes = (uint32_t)p.tables_bytes;

@@ -29,7 +29,8 @@ ENGINES = ("umma", "simt")
 
 
 def umma_ok(hop):
-    return (hop <= 64 and 64 % hop == 0) or (hop % 64 == 0 and hop <= 256) or hop % 256 == 0
+    # rows of lcm(hop, 64) <= 256 samples (hop | 64, hop | 192, 128, 256), or hop % 256 == 0
+    return math.lcm(hop, 64) <= 256 or hop % 256 == 0
 
 
 def engines_for(hop):
@@ -353,6 +354,22 @@ def test_pass_groups_are_byte_identical(groups, monkeypatch):
         split = plan.execute_host(x)
         plan.close()
         assert one.tobytes() == split.tobytes(), (cid, groups)
+
+
+@pytest.mark.parametrize("hop", [3, 6, 12, 24, 48, 96, 192])
+def test_hops_dividing_192_on_tensor_cores(hop):
+    """Hops whose rows are 192 samples (lcm(hop, 64) = 192: three 64-sample panels per row,
+    P = 192/hop frames per row) run on the tensor-core engine and match the oracle; hop 192
+    itself was accepted by the planner before row chunking handled non-power-of-two panels."""
+    x = synth.make_batch(2, clips=2, n=20000, start=2)
+    sc = synth.config_scales(2)
+    plan = wh.CwthPlan(sc, None, hop, 20000, wavelet="rmor", output="abs", max_clips=2, engine="auto")
+    assert plan.engine == "umma"
+    got = plan.execute_host(x)
+    plan.close()
+    ref = O.cwth_batch(x, sc, hop, wavelet="rmor", output="abs")
+    assert got.shape == (2, len(sc), -(-20000 // hop))
+    assert row_rel_err(got, ref) <= ROW_TOL
 
 
 @pytest.mark.parametrize("engine", ["umma", "simt"])
