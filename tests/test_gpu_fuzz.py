@@ -1,0 +1,18 @@
+"""Randomised parity sweep on the GPU (tools/fuzz.py): random hops (dividing 64 / 192, multiples
+of 64 / 256, and hops only the SIMT engine takes), lengths from 1 sample, scale grids, both
+wavelets, every output and min-max, AUTO and forced engines -- each case against the oracle."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_random_cases_match_oracle(seed):
+    p = subprocess.run([sys.executable, os.path.join(REPO, "tools", "fuzz.py"), "80", str(seed)],
+                       capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert p.returncode == 0 and "fuzz ok" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
