@@ -47,6 +47,7 @@ static constexpr int UM_CONV_THREADS = 32 * UM_CONV_WARPS;
 static constexpr int UM_EPI_WARPS = 8;  // 2 per TMEM lane quadrant
 static constexpr int UM_THREADS = 64 + UM_CONV_THREADS + 32 * UM_EPI_WARPS;  // producer, MMA, converters, epilogue
 static constexpr int UM_SLOTS = 16;  // in-flight tap tiles (ring slots)
+static constexpr int UM_PF = 2;     // converters prefetch windows this many units ahead (L2)
 static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
 
 struct UmmaArgs {
@@ -64,6 +65,7 @@ struct UmmaArgs {
     int32_t n_stream;                   // tap groups streamed through the ring every unit
     int32_t cpr, cpr_magic;             // 8-sample chunks per window row (panels * 8); ceil(2^20 / cpr)
     int32_t conv_regs;                  // converters prefetch the window into registers
+    int32_t pf;                         // converters prefetch windows into L2 ahead (rows of 256)
     const UmmaPass *passes;
     const UmmaTile *tiles;
     const UmmaGroup *groups;
@@ -761,6 +763,24 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(cv[i][k]));
         cmx = mx;
     };
+    // L2 prefetch of a unit's fp32 window (one bulk prefetch: the window is a contiguous sample
+    // range of one clip), issued UM_PF units ahead so that the converters' loads hit L2.  Only
+    // for rows of 256 samples (hop 256 / multiples of 256: one 147 KB window, its conversion not
+    // overlapped with the MMAs; c4 hop 256 / 1024 -6 %); neutral or slower elsewhere.
+    auto window_prefetch = [&](int64_t item) {
+        if (!A.pf || item >= n_units) return;
+        int64_t b, tile;
+        unit_tile(item, b, tile);
+        const int64_t w0 = tile * 128 * A.V - A.G0;
+        int64_t lo = w0 > 0 ? w0 : 0, hi = w0 + (int64_t)A.win_rows * A.V;
+        if (hi > A.N) hi = A.N;
+        if (hi <= lo) return;
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.x + b * A.ld_x + lo) & ~(uintptr_t)15;
+        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(A.x + b * A.ld_x + hi) + 15) & ~(uintptr_t)15;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+    };
+    if (threadIdx.x == 64)
+        for (int k = 1; k <= UM_PF; ++k) window_prefetch(u0 + k * ustride);
     if (warp >= 2 && warp < 2 + UM_CONV_WARPS && A.conv_regs && u0 < n_units) conv_fetch(u0);
     const uint32_t WH = A.win_half_bytes;               // bytes of one (hi or lo) window
     uint8_t *win_base = smem;                            // [win_bufs][hi|lo][panels][rows][128]
@@ -1067,7 +1087,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);
                 const int64_t in_hi64 = A.N - w0;
                 const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
-                if (ct == 0) WH_TRACE(3, wcnt);
+                if (ct == 0) {
+                    WH_TRACE(3, wcnt);
+                    window_prefetch(item + (UM_PF + 1) * ustride);
+                }
                 // this unit's window (the first one was fetched at launch)
                 if (item != u0) conv_fetch(item);
                 float (&v)[CONV_RC][8] = cv;
@@ -1153,7 +1176,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             const uint32_t wb = wcnt % A.win_bufs;
             int64_t slo, shi;
             staged(item, slo, shi);
-            if (ct == 0) WH_TRACE(3, wcnt);
+            if (ct == 0) {
+                WH_TRACE(3, wcnt);
+                window_prefetch(item + (UM_PF + 1) * ustride);
+            }
             if (A.use_stg) mbar_wait_p(&stg_full, wcnt & 1, pa, 0, pon);
             if (ct == 0) WH_TRACE(4, wcnt);
             // chunk c = 8 consecutive samples: (row, column chunk) = chunk_rc(c) (cpr = panels * 8
@@ -1931,6 +1957,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.res_bytes = (uint32_t)p.res_bytes;
     a.n_stream = p.n_stream;
     a.cpr = p.panels * 8;
+    a.pf = p.V >= 256 ? 1 : 0;
     a.cpr_magic = ((1 << 20) + a.cpr - 1) / a.cpr;
     a.conv_regs = (!p.use_stg && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
