@@ -696,13 +696,16 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     const int64_t n_units = A.clips * tpu * A.pgroups;
     // unit u: pass group u % pgroups of tile pair (u / pgroups) -- consecutive units (the pass
     // groups of one tile pair) go to different CTA pairs
+    // (32-bit index math: the launcher checks n_units < 2^31)
+    const uint32_t tpu32 = (uint32_t)tpu, pg32 = (uint32_t)A.pgroups;
     auto unit_tile = [&](int64_t u, int64_t &b, int64_t &tile) {
-        const int64_t v = u / A.pgroups;
-        b = v / tpu;
-        tile = CG * (v % tpu) + rank;
+        const uint32_t v = (uint32_t)u / pg32;
+        const uint32_t bq = v / tpu32;
+        b = (int64_t)bq;
+        tile = (int64_t)(CG * (v - bq * tpu32) + rank);
     };
     auto unit_passes = [&](int64_t u, int &p0, int &p1) {
-        p0 = (int)(u % A.pgroups) * A.ppu;
+        p0 = (int)((uint32_t)u % pg32) * A.ppu;
         p1 = p0 + A.ppu < A.n_passes ? p0 + A.ppu : A.n_passes;
     };
     // Converters, register-prefetch path: each thread loads its first CONV_RC 8-sample chunks
@@ -1493,15 +1496,15 @@ static UmmaKernel umma_kernel(int Cc, int P, int CG) {
 int umma_supported(const Plan &p, std::string *why) {
     const int64_t H = p.hop;
     const bool small = H <= 64 && 64 % H == 0;
-    const bool big = H % 64 == 0 && H <= 256;
-    const bool strided = H > 256 && H % 256 == 0;  // rows of 256 samples, every (H/256)-th a frame
+    const bool big = H % 64 == 0 && H < 256;
+    const bool strided = H >= 256 && H % 128 == 0;  // rows of 128 samples, every (H/128)-th a frame
     const int64_t lcm64 = H / std::gcd(H, (int64_t)64) * 64;
     const bool mid = !small && !big && !strided && lcm64 <= 256;  // 3, 6, 12, 24, 48, 96: rows of 192
     if (!small && !big && !strided && !mid) {
-        if (why) *why = "hop must divide 64 or 192, or be a multiple of 64 up to 256, or a multiple of 256";
+        if (why) *why = "hop must divide 64 or 192, or be 128 or 192, or a multiple of 128 from 256";
         return WH_E_UNSUPPORTED;
     }
-    const int64_t V = small ? 64 : (big ? H : (mid ? lcm64 : 256));
+    const int64_t V = small ? 64 : (big ? H : (mid ? lcm64 : 128));
     const int64_t P = strided ? 1 : V / H;
     const int64_t maxg = (p.Lmax + V - 1) / V * V + p.Lmax + (P - 1) * (strided ? 0 : H);  // longest K range
     const int64_t ksteps = maxg / 64 + 1;
@@ -1539,9 +1542,18 @@ int umma_prepare(Plan &p) {
     // still far ahead of the SIMT engine)
     int64_t H = p.hop;
     p.rs = 1;
-    if (H > 256) {
-        p.rs = (int32_t)(H / 256);
-        H = 256;
+    {
+        // hop >= 256, a multiple of 128: rows of R = 128 samples, every (hop/R)-th row a frame.
+        // Rows of 256 (one frame per row at hop 256) need a 147 KB window per tile that cannot
+        // be double-buffered: measured c4 hop 256 / 1024 274 / 260 us with rows of 256, 227 / 226
+        // with rows of 128 (2x the rows computed, windows half the size), 286 with rows of 64.
+        int64_t R = 128;
+        if (const char *r = std::getenv("WH_UMMA_ROW"))  // diagnostics: rows of 256 where hop % 256 == 0
+            if (std::atoi(r) == 256 && H % 256 == 0) R = 256;
+        if (H >= 256 && H % R == 0 && (H > 256 || R < 256)) {
+            p.rs = (int32_t)(H / R);
+            H = R;
+        }
     }
     // rows of V = lcm(hop, 64) samples (<= 256): hop | 64 -> 64, hop | 192 -> 192, hop = 128,
     // 192, 256 -> hop; P = V / hop frames (phases) per row
@@ -1996,6 +2008,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.ppu = (n_passes + G - 1) / G;
     a.pgroups = (n_passes + a.ppu - 1) / a.ppu;
     const int64_t units = tile_units * a.pgroups;
+    if (units >= ((int64_t)1 << 31)) return fail(WH_E_INVALID_ARG, "UMMA engine: too many clips for one launch");
     int64_t grid = std::min<int64_t>(units * p.cg, p.grid_ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls

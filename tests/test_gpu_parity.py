@@ -29,8 +29,9 @@ ENGINES = ("umma", "simt")
 
 
 def umma_ok(hop):
-    # rows of lcm(hop, 64) <= 256 samples (hop | 64, hop | 192, 128, 256), or hop % 256 == 0
-    return math.lcm(hop, 64) <= 256 or hop % 256 == 0
+    # rows of lcm(hop, 64) <= 192 samples (hop | 64, hop | 192, 128), or, from 256, rows of 128
+    # samples of which every (hop/128)-th is a frame (multiples of 128)
+    return (math.lcm(hop, 64) <= 256 and hop < 256) or (hop >= 256 and hop % 128 == 0)
 
 
 def engines_for(hop):
