@@ -442,11 +442,19 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
     int64_t max_chunks = 8;
     if (const char *c = std::getenv("WH_HOST_CHUNKS")) max_chunks = std::max(1, std::atoi(c));  // experiments
     const int64_t n_chunks = (pinned && clips >= 4) ? std::min<int64_t>(max_chunks, clips) : 1;
-    const int64_t per = (clips + n_chunks - 1) / n_chunks;
+    // The D2H copies bound the pipeline; the first chunk is small so that they start early
+    // (its H2D copy and kernel are the pipeline fill), the rest are equal.
+    int64_t first = clips, per = clips;
+    if (n_chunks > 1) {
+        first = std::max<int64_t>(1, clips / (4 * n_chunks));
+        if (const char *f = std::getenv("WH_HOST_FIRST")) first = std::max<int64_t>(1, std::atoi(f));  // experiments
+        first = std::min(first, clips - (n_chunks - 1));
+        per = (clips - first + n_chunks - 2) / (n_chunks - 1);
+    }
     const size_t out_clip = (size_t)p->S * p->F * out_elem_bytes(*p);
     int rc = WH_OK;
-    for (int64_t c0 = 0, j = 0; c0 < clips && rc == WH_OK; c0 += per, ++j) {
-        const int64_t nc = std::min(per, clips - c0);
+    for (int64_t c0 = 0, j = 0, nc = first; c0 < clips && rc == WH_OK; c0 += nc, ++j, nc = per) {
+        nc = std::min(nc, clips - c0);
         cudaStream_t s = (j & 1) ? p->stream2 : p->stream;
         float *dx = p->d_x + (size_t)c0 * p->N;
         uint8_t *dout = reinterpret_cast<uint8_t *>(p->d_out) + (size_t)c0 * out_clip;
