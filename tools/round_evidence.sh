@@ -15,3 +15,7 @@ timeout 120 python tools/run_plan.py --iters 2 > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_umma -s 1 -c 1 \
     -o gpurun_out/prof_umma_c2_${TAG} python tools/run_plan.py --iters 2 > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
 tail -c 600 gpurun_out/bench_c2_${TAG}.json; echo; tail -c 300 gpurun_out/bench_c5_${TAG}.json
+bash tools/sweep.sh ${TAG}_sweep > gpurun_out/sweep_${TAG}.txt 2>&1; echo "sweep rc=$?"
+cat gpurun_out/sweep_${TAG}.txt
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests_${TAG}.log 2>&1; echo "gpu tests rc=$?"; tail -2 gpurun_out/gpu_tests_${TAG}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_${TAG}.log
