@@ -6,11 +6,12 @@
 // with the zero padding of wavelet.py:243-246 made implicit (out-of-range samples read 0).
 //
 // Tiling: one CTA = (clip, group of <= 8 consecutive scales, tile of tf frames).  The
-// clip segment the tile touches is staged once in shared memory.  Each warp owns 4
-// frames x 8 scales; its 32 lanes split the tap index j (j = lane + 32 t), so the
-// segment reads x[c +- j] are consecutive across lanes (conflict-free for any hop) and
-// the tap reads are coalesced 128 B lines.  The 32 (or 64, complex) partial sums are
-// combined with a 31-shuffle transpose-reduction so lane l ends with output l.
+// clip segment the tile touches is staged once in shared memory.  Each warp owns 8 frames
+// (4 for complex) x 8 scales; its 32 lanes split the tap index j (j = lane + 32 t), so the
+// segment reads x[c +- j] are consecutive across lanes (conflict-free for any hop) and a
+// lane reads the 8 scales' taps at its j with two 16-byte loads (table [j][8]).  Each block
+// of 4 frames x 8 scales (x re / im) is combined with a 31-shuffle transpose-reduction so
+// lane l ends with output l.
 #include <algorithm>
 
 #include "wh_internal.h"
@@ -27,14 +28,16 @@ __global__ void k_group_taps(const float *fold, const int64_t *fold_off, const i
     int32_t g = blockIdx.y;
     if (g >= n_groups) return;
     SimtGroup G = groups[g];
+    // [j][SIMT_G] (re table, then im): the 8 scales' taps at one j are 32 contiguous bytes,
+    // two 16-byte loads per lane; scales >= ns are zero
     int64_t width = G.L + 1;
-    int64_t n = (int64_t)G.ns * width;
+    int64_t n = (int64_t)SIMT_G * width;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int s = (int)(i / width);
-        int64_t j = i % width;
+        int s = (int)(i % SIMT_G);
+        int64_t j = i / SIMT_G;
         int sg = G.s0 + s;
-        bool in = j <= half[sg];
+        bool in = s < G.ns && j <= half[sg];
         gt[G.tap_off + i] = in ? fold[fold_off[sg] + j] : 0.0f;
         gt[G.tap_off + n + i] = in ? fold[fold_total + fold_off[sg] + j] : 0.0f;
     }
@@ -80,56 +83,74 @@ k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int width = L + 1;
     const float *tre = gtaps + G.tap_off;
-    const float *tim = tre + (int64_t)G.ns * width;
+    const float *tim = tre + (int64_t)SIMT_G * width;
     float lmin = INFINITY, lmax = -INFINITY;
 
-    for (int fq = warp * 4; fq < nf; fq += 4 * (SIMT_THREADS / 32)) {
-        float ar[32], ai[32];
+    // FW frames x 8 scales per warp (real: 8 frames, complex: 4 frames and re + im)
+    constexpr int FW = CPLX ? 4 : 8;
+    constexpr int NA = FW * SIMT_G;  // accumulators per lane (re)
+    for (int fq = warp * FW; fq < nf; fq += FW * (SIMT_THREADS / 32)) {
+        float ar[NA], ai[CPLX ? NA : 1];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            ar[i] = 0.0f;
-            ai[i] = 0.0f;
+        for (int i = 0; i < NA; ++i) ar[i] = 0.0f;
+        if constexpr (CPLX) {
+#pragma unroll
+            for (int i = 0; i < NA; ++i) ai[i] = 0.0f;
         }
-        int c[4];
+        int c[FW];
 #pragma unroll
-        for (int f = 0; f < 4; ++f) c[f] = min(fq + f, nf - 1) * (int)hop + L;
+        for (int f = 0; f < FW; ++f) c[f] = min(fq + f, nf - 1) * (int)hop + L;
+        const float4 *tr4 = reinterpret_cast<const float4 *>(tre);
+        const float4 *ti4 = reinterpret_cast<const float4 *>(tim);
         for (int j = lane; j <= L; j += 32) {
-            float p[4], d[4];
+            float p[FW], d[FW];
 #pragma unroll
-            for (int f = 0; f < 4; ++f) {
+            for (int f = 0; f < FW; ++f) {
                 float xp = xs[c[f] + j], xm = xs[c[f] - j];
                 p[f] = (j == 0) ? xp : xp + xm;
                 d[f] = xp - xm;
             }
+            const float4 ta = __ldg(tr4 + 2 * j), tb = __ldg(tr4 + 2 * j + 1);
+            const float t[SIMT_G] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
 #pragma unroll
-            for (int s = 0; s < SIMT_G; ++s) {
-                if (s < G.ns) {
-                    float tr = __ldg(tre + s * width + j);
+            for (int s2 = 0; s2 < SIMT_G; ++s2)
 #pragma unroll
-                    for (int f = 0; f < 4; ++f) ar[f * 8 + s] = fmaf(p[f], tr, ar[f * 8 + s]);
-                    if constexpr (CPLX) {
-                        float ti = __ldg(tim + s * width + j);
+                for (int f = 0; f < FW; ++f) ar[f * SIMT_G + s2] = fmaf(p[f], t[s2], ar[f * SIMT_G + s2]);
+            if constexpr (CPLX) {
+                const float4 ua = __ldg(ti4 + 2 * j), ub = __ldg(ti4 + 2 * j + 1);
+                const float u[SIMT_G] = {ua.x, ua.y, ua.z, ua.w, ub.x, ub.y, ub.z, ub.w};
 #pragma unroll
-                        for (int f = 0; f < 4; ++f) ai[f * 8 + s] = fmaf(d[f], ti, ai[f * 8 + s]);
-                    }
-                }
+                for (int s2 = 0; s2 < SIMT_G; ++s2)
+#pragma unroll
+                    for (int f = 0; f < FW; ++f) ai[f * SIMT_G + s2] = fmaf(d[f], u[s2], ai[f * SIMT_G + s2]);
             }
         }
-        float re = transpose_reduce32(ar, lane);
-        float im = 0.0f;
-        if constexpr (CPLX) im = transpose_reduce32(ai, lane);
-        const int f = lane >> 3, s = lane & 7;
-        const int64_t k = k0 + fq + f;
-        if (s < G.ns && fq + f < nf) {
-            const int64_t o = (b * S + G.s0 + s) * F + k;
-            if (output == WH_OUT_COMPLEX64) {
-                reinterpret_cast<float2 *>(out)[o] =
-                    make_float2(re, wavelet == WH_WAVELET_RMOR ? 0.0f : im);
-            } else {
-                float v = apply_output(magnitude(re, im, wavelet), output);
-                reinterpret_cast<float *>(out)[o] = v;
-                lmin = fminf(lmin, v);
-                lmax = fmaxf(lmax, v);
+        // 32 partial sums per block of 4 frames x 8 scales -> lane l holds (frame l >> 3, scale l & 7)
+#pragma unroll
+        for (int h = 0; h < FW / 4; ++h) {
+            float blk[32], bim[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) blk[i] = ar[32 * h + i];
+            float re = transpose_reduce32(blk, lane);
+            float im = 0.0f;
+            if constexpr (CPLX) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) bim[i] = ai[32 * h + i];
+                im = transpose_reduce32(bim, lane);
+            }
+            const int f = 4 * h + (lane >> 3), s = lane & 7;
+            const int64_t k = k0 + fq + f;
+            if (s < G.ns && fq + f < nf) {
+                const int64_t o = (b * S + G.s0 + s) * F + k;
+                if (output == WH_OUT_COMPLEX64) {
+                    reinterpret_cast<float2 *>(out)[o] =
+                        make_float2(re, wavelet == WH_WAVELET_RMOR ? 0.0f : im);
+                } else {
+                    float v = apply_output(magnitude(re, im, wavelet), output);
+                    reinterpret_cast<float *>(out)[o] = v;
+                    lmin = fminf(lmin, v);
+                    lmax = fmaxf(lmax, v);
+                }
             }
         }
     }
@@ -165,7 +186,7 @@ int simt_prepare(Plan &p) {
         tf = std::max<int64_t>(1, std::min<int64_t>(tf, p.F));
         G.tf = (int32_t)tf;
         G.tap_off = tap_off;
-        tap_off += 2 * (int64_t)G.ns * (L + 1);
+        tap_off += 2 * (int64_t)SIMT_G * (L + 1);
         p.groups.push_back(G);
     }
     std::vector<int> order(p.groups.size());
