@@ -35,8 +35,8 @@ struct SimtGroup {      // a group of <= 8 consecutive scales sharing a tap tabl
     int32_t tf;         // frames per CTA tile
     int64_t tap_off;    // offset (floats) of the group's [ns][L+1] re table (im follows)
 };
-struct SimtItem {       // one CTA of work: group g, frames [k0, k0 + tf)
-    int32_t g, k0;
+struct SimtItem {       // one CTA of work: groups [g0, g1) of the cost-ordered list, frames [k0, k0 + tf)
+    int32_t g0, g1, k0, L;  // L: max half width over the groups (staged segment margin)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -108,6 +108,7 @@ struct Plan {
     float *d_scale_pow = nullptr;  // per scale 2^-f_s
     uint8_t *d_tables = nullptr;   // UMMA: the kernel's smem tables, packed (one bulk copy)
     int64_t tables_bytes = 0;
+    int32_t simt_tf = 1;           // SIMT: frames per item tile
     double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
     std::vector<int32_t> fexp;
     int32_t bstages = 2, win_bufs = 2;     // bstages: full-width tiles the ring holds (info)

@@ -63,16 +63,16 @@ __global__ void __launch_bounds__(SIMT_THREADS)
 k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_t F,
        const SimtGroup *__restrict__ groups, const SimtItem *__restrict__ items,
        const float *__restrict__ gtaps, int32_t S, int32_t wavelet, int32_t output,
-       void *__restrict__ out, uint32_t *__restrict__ minmax) {
+       void *__restrict__ out, uint32_t *__restrict__ minmax, int32_t tf_all) {
     extern __shared__ float xs[];
     const int64_t b = blockIdx.x;
     const SimtItem it = items[blockIdx.y];
-    const SimtGroup G = groups[it.g];
-    const int L = G.L;
+    // the segment is staged once for all the item's scale groups (margin = their max L)
+    const int LM = it.L;
     const int64_t k0 = it.k0;
-    const int nf = (int)(F - k0 < (int64_t)G.tf ? F - k0 : (int64_t)G.tf);
-    const int64_t seg_start = k0 * hop - L;
-    const int64_t seg_len = (int64_t)(nf - 1) * hop + 2 * L + 1;
+    const int nf = (int)(F - k0 < (int64_t)tf_all ? F - k0 : (int64_t)tf_all);
+    const int64_t seg_start = k0 * hop - LM;
+    const int64_t seg_len = (int64_t)(nf - 1) * hop + 2 * LM + 1;
     const float *xb = x + b * ld_x;
     for (int64_t i = threadIdx.x; i < seg_len; i += SIMT_THREADS) {
         int64_t g = seg_start + i;
@@ -81,10 +81,13 @@ k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float lmin = INFINITY, lmax = -INFINITY;
+    for (int gi = it.g0; gi < it.g1; ++gi) {
+    const SimtGroup G = groups[gi];
+    const int L = G.L;
     const int width = L + 1;
     const float *tre = gtaps + G.tap_off;
     const float *tim = tre + (int64_t)SIMT_G * width;
-    float lmin = INFINITY, lmax = -INFINITY;
 
     // FW frames x 8 scales per warp (real: 8 frames, complex: 4 frames and re + im)
     constexpr int FW = CPLX ? 4 : 8;
@@ -99,7 +102,7 @@ k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_
         }
         int c[FW];
 #pragma unroll
-        for (int f = 0; f < FW; ++f) c[f] = min(fq + f, nf - 1) * (int)hop + L;
+        for (int f = 0; f < FW; ++f) c[f] = min(fq + f, nf - 1) * (int)hop + LM;
         const float4 *tr4 = reinterpret_cast<const float4 *>(tre);
         const float4 *ti4 = reinterpret_cast<const float4 *>(tim);
         for (int j = lane; j <= L; j += 32) {
@@ -154,6 +157,7 @@ k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_
             }
         }
     }
+    }  // scale groups
     if (minmax) {
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
@@ -189,13 +193,40 @@ int simt_prepare(Plan &p) {
         tap_off += 2 * (int64_t)SIMT_G * (L + 1);
         p.groups.push_back(G);
     }
+    // groups in decreasing cost (L) order, split into up to SIMT_CHUNKS contiguous chunks of
+    // about equal tap work; an item = (chunk, frame tile): the clip segment is staged once per
+    // item for all its groups (staging it per group re-read the input ~16x for short taps)
     std::vector<int> order(p.groups.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(),
                      [&](int a, int b) { return p.groups[a].L > p.groups[b].L; });
+    std::vector<SimtGroup> sorted;
+    for (int g : order) sorted.push_back(p.groups[g]);
+    p.groups = sorted;
+    double work_total = 0.0;
+    for (auto &G : p.groups) work_total += (double)(G.L + 1);
+    constexpr int SIMT_CHUNKS = 4;
+    std::vector<int> cuts{0};
+    double acc = 0.0;
+    for (size_t g = 0; g < p.groups.size(); ++g) {
+        acc += (double)(p.groups[g].L + 1);
+        if ((int)cuts.size() < SIMT_CHUNKS && acc >= work_total * (double)cuts.size() / SIMT_CHUNKS && g + 1 < p.groups.size())
+            cuts.push_back((int)g + 1);
+    }
+    cuts.push_back((int)p.groups.size());
+    int64_t Lmax_all = 0;
+    for (auto &G : p.groups) Lmax_all = std::max<int64_t>(Lmax_all, G.L);
+    int64_t tf = (SIMT_SEG_MAX - 2 * Lmax_all - 1) / p.hop + 1;
+    tf = std::min<int64_t>(tf, 128);
+    if (tf >= 16) tf = tf / 16 * 16;
+    tf = std::max<int64_t>(1, std::min<int64_t>(tf, p.F));
+    p.simt_tf = (int32_t)tf;
     std::vector<SimtItem> items;
-    for (int g : order)
-        for (int64_t k0 = 0; k0 < p.F; k0 += p.groups[g].tf) items.push_back(SimtItem{g, (int32_t)k0});
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+        if (cuts[c] == cuts[c + 1]) continue;
+        const int32_t Lc = p.groups[cuts[c]].L;  // the chunk's first group is its largest
+        for (int64_t k0 = 0; k0 < p.F; k0 += tf) items.push_back(SimtItem{cuts[c], cuts[c + 1], (int32_t)k0, Lc});
+    }
     if (items.size() > 65535u) return fail(WH_E_UNSUPPORTED, "too many SIMT work items");
     p.n_items = (int32_t)items.size();
     WH_CUDA_TRY(cudaMalloc(&p.d_groups, sizeof(SimtGroup) * p.groups.size()));
@@ -208,9 +239,7 @@ int simt_prepare(Plan &p) {
     k_group_taps<<<grid, 256>>>(p.d_fold, p.d_fold_off, p.d_half, p.fold_total, p.d_groups,
                                 (int32_t)p.groups.size(), p.d_group_taps);
     WH_CUDA_TRY(cudaGetLastError());
-    size_t smem = 0;
-    for (auto &G : p.groups)
-        smem = std::max<size_t>(smem, sizeof(float) * ((int64_t)(G.tf - 1) * p.hop + 2 * G.L + 1));
+    const size_t smem = sizeof(float) * ((size_t)(tf - 1) * p.hop + 2 * Lmax_all + 1);
     p.smem_bytes = smem;
     WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -225,10 +254,10 @@ int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     if (cplx)
         k_simt<true><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
-                                                             p.d_group_taps, p.S, p.wavelet, p.output, out, mm);
+                                                             p.d_group_taps, p.S, p.wavelet, p.output, out, mm, p.simt_tf);
     else
         k_simt<false><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
-                                                              p.d_group_taps, p.S, p.wavelet, p.output, out, mm);
+                                                              p.d_group_taps, p.S, p.wavelet, p.output, out, mm, p.simt_tf);
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }
