@@ -1740,7 +1740,12 @@ int umma_prepare(Plan &p) {
         }
     }
     p.resident = t_split > 0 ? 1 : 0;
-    const int64_t group_target = p.resident ? 48 * 1024 : (n_tiles >= 64 ? 48 * 1024 : 24 * 1024);
+    // Streamed banks: tap groups of up to 48 KB.  Short unit sequences (< 64 tiles) keep two
+    // windows (no fp32 staging, register converter), with groups as large as a ring of three
+    // fits beside them (c4 hop 16: 24 KB groups + staging 558 us, 44 KB + two windows 456 us);
+    // long ones keep one window and 48 KB groups (c5, c3, c4 hop 1: measured best).
+    const int64_t two_win_groups = std::min<int64_t>(48 * 1024, (budget0 - 2 * win) / 3 / 1024 * 1024);
+    const int64_t group_target = p.resident ? 48 * 1024 : (n_tiles >= 64 ? 48 * 1024 : std::max<int64_t>(16 * 1024, two_win_groups));
     int64_t group_target_env = 0;
     if (const char *g = std::getenv("WH_UMMA_GROUP_KB")) group_target_env = std::max(1, std::atoi(g)) * 1024;
     p.groups_u.clear();
@@ -1829,7 +1834,7 @@ int umma_prepare(Plan &p) {
         ring = res_bytes + rest;
     } else {
         const int prefer_single = n_tiles >= 64 && std::getenv("WH_UMMA_PREFER_DOUBLE") == nullptr;
-        const int opts_a[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
+        const int opts_a[4][2] = {{2, 0}, {2, 1}, {1, 1}, {1, 0}};
         const int opts_b[4][2] = {{1, 1}, {2, 1}, {1, 0}, {2, 0}};
         const int (*opts)[2] = prefer_single ? opts_b : opts_a;
         const char *force = std::getenv("WH_UMMA_SMEM_OPT");  // diagnostics: force an option
