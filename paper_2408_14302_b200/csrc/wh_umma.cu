@@ -1996,17 +1996,29 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     const int64_t tile_units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
     const int64_t pairs = std::max<int64_t>(1, p.grid_ctas / p.cg);
     const int n_passes = (int)p.passes.size();
+    // Among splits within 3 % of the best modelled time, the one whose last round of units is
+    // fullest wins (c3: 11 groups of 3 passes, last round 66 / 74 full: 150 us; 8 groups of 4,
+    // 48 / 74: 165 us; 16 groups of 2, 22 / 74: 163 us -- all model the same 36 pass-rounds).
     int G = 1;
-    double best = -1.0;
+    double best = -1.0, best_fill = -1.0;
+    std::vector<std::pair<int, double>> cand;  // (G, modelled time)
     for (int g = 1; g <= n_passes; ++g) {
         const int ppu = (n_passes + g - 1) / g;
         const int gg = (n_passes + ppu - 1) / ppu;  // groups actually formed
         if (gg != g) continue;
         const double rounds = std::ceil((double)(tile_units * g) / (double)pairs);
         const double t = rounds * std::max(p.unit_cost * (double)ppu / n_passes, 6000.0);
-        if (best < 0 || t < best * 0.97) {
-            best = t;
-            G = g;
+        cand.emplace_back(g, t);
+        if (best < 0 || t < best) best = t;
+    }
+    // (only when there are few tile pairs; otherwise the first split within 3 % of the best)
+    for (auto &c : cand) {
+        if (c.second > best * 1.03) continue;
+        const int64_t rem = (tile_units * c.first) % pairs;
+        const double fill = rem == 0 ? 1.0 : (double)rem / (double)pairs;
+        if (best_fill < 0.0 || (tile_units < 4 * pairs && fill > best_fill + 1e-9)) {
+            G = c.first;
+            best_fill = fill;
         }
     }
     if (const char *e = std::getenv("WH_UMMA_PGROUPS")) G = std::max(1, std::min(n_passes, std::atoi(e)));
