@@ -109,6 +109,7 @@ struct Plan {
     uint8_t *d_tables = nullptr;   // UMMA: the kernel's smem tables, packed (one bulk copy)
     int64_t tables_bytes = 0;
     int32_t simt_tf = 1;           // SIMT: frames per item tile
+    bool doubled_v = false, no_2v = false;  // UMMA: rows of 2 lcm(hop, 64) samples (one pass)
     double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
     std::vector<int32_t> fexp;
     int32_t bstages = 2, win_bufs = 2;     // bstages: full-width tiles the ring holds (info)

@@ -1535,7 +1535,18 @@ static int ncheck_tiles(const Plan &p) {
     return WH_OK;
 }
 
+static int umma_prepare_impl(Plan &p);
 int umma_prepare(Plan &p) {
+    // a plan with doubled rows that does not fit shared memory is planned again without
+    p.no_2v = false;
+    int rc = umma_prepare_impl(p);
+    if (rc == WH_E_UNSUPPORTED && p.doubled_v) {
+        p.no_2v = true;
+        rc = umma_prepare_impl(p);
+    }
+    return rc;
+}
+static int umma_prepare_impl(Plan &p) {
     // hop | 64: rows of 64 samples, P = 64/hop frames (phases) per row; hop = 64..256 (multiple
     // of 64): one frame per row of hop samples; hop = 256*RS: rows of 256 samples of which
     // every RS-th is a frame (the other rows are computed and dropped: RS x the tensor work,
@@ -1558,6 +1569,15 @@ int umma_prepare(Plan &p) {
     // rows of V = lcm(hop, 64) samples (<= 256): hop | 64 -> 64, hop | 192 -> 192, hop = 128,
     // 192, 256 -> hop; P = V / hop frames (phases) per row
     p.V = (int32_t)(H / std::gcd(H, (int64_t)64) * 64);
+    {
+        // Twice the phases per row when the columns still fit one pass: each A-operand read then
+        // serves twice the columns (c4 hop 64, 64 scales: 285 -> 228 us, the bank streamed
+        // beside two windows); with more columns the second pass re-reads A (c2: 65 -> 110 us)
+        const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
+        p.doubled_v = p.rs == 1 && 2 * p.V <= 256 && 2 * (p.V / H) * cc * (int64_t)p.S <= 128 && !p.no_2v &&
+                      std::getenv("WH_UMMA_V") == nullptr && std::getenv("WH_UMMA_NO_2V") == nullptr;
+        if (p.doubled_v) p.V *= 2;
+    }
     if (const char *v = std::getenv("WH_UMMA_V")) {  // experiment: more phases per row
         const int vv = std::atoi(v);
         if (vv >= p.V && vv % 64 == 0 && vv % H == 0 && p.rs == 1) p.V = vv;
