@@ -1,6 +1,7 @@
 """Randomised parity sweep on the GPU (tools/fuzz.py): random hops (dividing 64 / 192, multiples
 of 64 / 256, and hops only the SIMT engine takes), lengths from 1 sample, scale grids, both
-wavelets, every output and min-max, AUTO and forced engines -- each case against the oracle."""
+wavelets, every output and min-max, AUTO and forced engines -- each case against the oracle;
+"big" cases use full-length clips (160,000+ samples)."""
 import os
 import subprocess
 import sys
@@ -11,8 +12,8 @@ pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("seed", [11, 12])
-def test_random_cases_match_oracle(seed):
-    p = subprocess.run([sys.executable, os.path.join(REPO, "tools", "fuzz.py"), "80", str(seed)],
-                       capture_output=True, text=True, timeout=600, cwd=REPO)
+@pytest.mark.parametrize("seed,cases,mode", [(11, 80, ""), (12, 80, ""), (13, 20, "big")])
+def test_random_cases_match_oracle(seed, cases, mode):
+    args = [sys.executable, os.path.join(REPO, "tools", "fuzz.py"), str(cases), str(seed)] + ([mode] if mode else [])
+    p = subprocess.run(args, capture_output=True, text=True, timeout=600, cwd=REPO)
     assert p.returncode == 0 and "fuzz ok" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]

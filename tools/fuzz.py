@@ -14,6 +14,7 @@ from oracle import oracle as O  # noqa: E402
 
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 120
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+big = len(sys.argv) > 3 and sys.argv[3] == "big"  # full-length clips (160,000+ samples), hop >= 32
 hop_pool = [1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 31, 32, 48, 50, 64, 96, 100, 127, 128, 160, 192, 200, 255,
             256, 300, 384, 512, 640, 768, 1024, 1500]
 t_start = time.time()
@@ -25,6 +26,11 @@ for i in range(n_cases):
     s_count = int(rng.integers(1, 48))
     a0 = float(rng.uniform(0.5, 4.0))
     a1 = float(a0 * rng.uniform(1.0, 120.0))
+    if big:
+        hop = int(rng.choice([h for h in hop_pool if h >= 32]))
+        n = int(rng.choice([160000, 160001, 300007]))
+        clips = int(rng.integers(1, 3))
+        a1 = float(min(a1, 130.0))
     scales = np.unique(np.geomspace(a0, a1, s_count))
     wavelet = str(rng.choice(["cmor", "rmor"]))
     output = str(rng.choice(["complex", "abs", "power", "log1p", "log_db"]))
