@@ -192,9 +192,14 @@ def run_reference(args, w):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded MIMII stand-in, SURVEY.md §8d)",
-        "config": {"workload": w["name"], "clips": sample, "n_samples": w["n"],
-                   "scales": len(w["scales"]), "hop": w["hop"], "wavelet": w["wavelet"],
-                   "output": w["output"], "norm": w["norm"]},
+        # the same keys as the GPU arm's config; a step is `sample` clips (the whole per-GPU
+        # batch for c2) on the host cores
+        "config": {"workload": w["name"], "clips_per_gpu": sample, "n_samples": w["n"],
+                   "scales": len(w["scales"]), "scale_range": [float(w["scales"][0]),
+                                                              float(w["scales"][-1])],
+                   "hop": w["hop"], "wavelet": w["wavelet"], "output": w["output"],
+                   "norm": w["norm"], "engine": "cpu-oracle-port", "parallelism": f"host threads x{threads}",
+                   "l2": "n/a (host)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{sample} clips of {w['name']} per step, oracle/wh_oracle.c "
                                    f"folded f64 kernel (numba-equivalent), {threads} threads"},
