@@ -1,23 +1,31 @@
 #!/usr/bin/env python
 """bench.py -- CWTH scalogram coefficients/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-One "step" = one pass of the hot path (cwth_batch with the config's fused epilogue) over
-the rank's batch of synthetic clips.  Default workload: BASELINE config 2 (configs[1]):
-64 clips x 160,000 fp32 samples of synthetic machine noise per GPU, real Morlet, 128
-geometric scales 1-128, hop 64, log1p(|W|).  N>1 (torchrun, one process per GPU): every
-rank processes its own 64 clips -- clips are independent, no data-path collective
-(weak scaling).  ``--config c5`` runs config 5 (4096 clips split across ranks, strong
-scaling).
+One "step" = one pass of the hot path (the plan's fused kernels) over the job's batch of
+synthetic clips.  Default workload: BASELINE config 5 -- the configuration the metric is
+quoted on ("at 1/2/4/8 B200"): 4096 clips x 160,000 fp32 samples of synthetic machine
+noise, complex Morlet (C = 1.0, B = 1.5), 160 geometric scales 1-512, hop 32, |W| with
+per-clip min-max normalisation.  It fits one B200 (2.6 GB in, 13.1 GB out), so N = 1 runs
+all 4096 clips; N > 1 splits the same 4096 clips into contiguous ranges, one per rank
+(strong scaling, no data-path collective).  ``--config c2`` etc. run the other configs
+(c1-c4 weak: the config's batch per GPU).
 
-Printed JSON (rank 0, one line): value = coeffs/s of the whole job from CUDA-event kernel
-time with inputs resident in HBM (L2 flushed by a 256 MiB write before every step);
-e2e = the same metric through the public API with pinned HOST buffers (H2D + kernels +
-D2H inside the timed region); roofline = the main kernel against its binding roof:
-algorithmic FLOP/s vs the measured bf16 tensor peak, or algorithmic bytes/s vs the measured
-HBM bandwidth, whichever bounds the algorithm (c2: HBM); cpu_baseline = the oracle port (oracle/) on the box's
-host cores, on the same clips.  ``--impl reference`` times only the CPU reference port.
+Multi-GPU: one process per GPU.  Under torchrun (WORLD_SIZE set) each rank runs its shard;
+without it, ``--gpus N`` (N > 1) re-executes this script under torch.distributed.run with N
+processes itself.  Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA
+events on the launch stream with the L2 flushed (256 MiB write) before every step; barrier +
+synchronize on both sides; the max over ranks is reported.
+
+Printed JSON (rank 0, one line): value = coeffs/s of the whole job, inputs resident in HBM;
+e2e = the same metric through the public API (CwthPlan.execute_host -> wh_execute_host)
+with pinned HOST buffers (H2D + kernels + D2H inside the timed region); roofline = the
+dominant kernel against its binding roof (c5: tensor, algorithmic flops vs the measured
+bf16 peak; c2: HBM); cpu_baseline = the CPU port of the reference (oracle/) on the box's
+host cores plus the unmodified reference package (baseline/_ref) on the same clips, and an
+untimed parity check of sampled clips of the timed output against the oracle.
+``--impl reference`` times only the reference's CPU path.
 """
 
 from __future__ import annotations
@@ -25,6 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,6 +50,8 @@ from paper_2408_14302_b200 import synth  # noqa: E402
 METRIC = "CWTH scalogram coeffs/sec (clips x scales x frames)"
 UNIT = "coeffs/s"
 L2_FLUSH_BYTES = 256 << 20
+DEFAULT_CONFIG = "c5"
+REF_PATH = os.path.join(REPO, "baseline", "_ref")
 
 
 def workload(name: str):
@@ -52,19 +63,23 @@ def workload(name: str):
         key, hop_override = "c4", int(name[3:])
     cid = base[key]
     cfg = dict(synth.CONFIGS[cid])
-    w = dict(cfg_id=cid, name=name, clips=cfg["clips"], n=cfg["n"],
-             scales=synth.config_scales(cid), hop=hop_override or cfg["hop"],
-             wavelet=cfg["wavelet"], output=cfg["output"], norm=cfg["norm"],
-             scaling="strong" if cid == 5 else "weak")
-    return w
+    return dict(cfg_id=cid, name=name, clips=cfg["clips"], n=cfg["n"],
+                scales=synth.config_scales(cid), hop=hop_override or cfg["hop"],
+                wavelet=cfg["wavelet"], output=cfg["output"], norm=cfg["norm"],
+                scaling="strong" if cid == 5 else "weak")
+
+
+def half_widths(w) -> np.ndarray:
+    """L_s = ceil(R a sqrt(B/2)) in float64 (wavelet.py:154), R = 6, B = 1.5."""
+    import math
+
+    return np.array([math.ceil(6.0 * float(a) * math.sqrt(1.5 / 2.0)) for a in w["scales"]])
 
 
 def alg_flops(w, clips: int) -> float:
     """unfolded direct correlation, 2*T (real) or 4*T (complex) flop/coeff."""
-    from oracle import oracle as O  # only for the integer half widths (same fp64 formula)
-
     F = -(-w["n"] // w["hop"])
-    T = np.array([2 * O.half_width(s) + 1 for s in w["scales"]], dtype=np.float64)
+    T = 2.0 * half_widths(w) + 1.0
     per = 2.0 if w["wavelet"] == "rmor" else 4.0
     return float(clips) * F * per * T.sum()
 
@@ -74,7 +89,17 @@ def coeffs(w, clips: int) -> float:
 
 
 def make_inputs(w, clips: int, start: int) -> np.ndarray:
-    return synth.make_batch(w["cfg_id"], clips=clips, n=w["n"], start=start)
+    """The rank's clips, generated in a thread pool (numpy's FFT releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    x = np.empty((clips, w["n"]), dtype=np.float32)
+
+    def one(c):
+        x[c] = synth.make_clip(w["cfg_id"], start + c, w["n"])
+
+    with ThreadPoolExecutor(max(1, min(32, len(os.sched_getaffinity(0))))) as ex:
+        list(ex.map(one, range(clips)))
+    return x
 
 
 def peaks():
@@ -152,8 +177,35 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_reference(w, x: np.ndarray, threads: int):
-    """Time the CPU port of the reference (oracle/) on clips x: returns seconds."""
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn(args) -> int:
+    """``--gpus N`` without torchrun: re-execute this script under torch.distributed.run
+    with one process per GPU (rank 0 prints the JSON line)."""
+    env = dict(os.environ)
+    # NCCL init logging (stderr) so the ranks and their devices are visible in the log
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+# ---------------------------------------------------------------------------------------
+# CPU legs (the only places bench.py executes oracle/ or the reference)
+# ---------------------------------------------------------------------------------------
+
+def port_time(w, x: np.ndarray, threads: int) -> float:
+    """Time the CPU port of the reference (oracle/wh_oracle.c) on clips x: seconds."""
     from oracle import oracle as O
 
     t0 = time.perf_counter()
@@ -174,8 +226,117 @@ def cpu_reference(w, x: np.ndarray, threads: int):
     return time.perf_counter() - t0
 
 
+def _ref_worker_init(path, disable_numba):
+    os.environ["WAVEHOP_DISABLE_NUMBA"] = "1" if disable_numba else "0"
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/wh_numba_cache")
+    os.environ["OMP_NUM_THREADS"] = "1"
+    sys.path.insert(0, path)
+
+
+def _ref_clip(task):
+    """One clip through the UNMODIFIED reference (cwth_strided, wavelet.py:215-273) plus the
+    config's epilogue in float64 (scalogram.py:51-83 semantics; real Morlet = real part)."""
+    x, scales, hop, wavelet, output, norm = task
+    from wavehop import MorletParams, ScaleGrid, SignalBuffer, cwth_strided
+
+    v = cwth_strided(SignalBuffer(x.astype(np.float64), 16000.0), ScaleGrid(np.asarray(scales)),
+                     MorletParams(), int(hop), threads=1).values
+    m = np.abs(v.real) if wavelet == "rmor" else np.abs(v)
+    if output == "power":
+        m = m * m
+    elif output == "log1p":
+        m = np.log1p(m)
+    elif output == "log_db":
+        m = 20.0 * np.log10(m + 1e-12)
+    if norm == "minmax":
+        lo, hi = m.min(), m.max()
+        m = np.zeros_like(m) if hi == lo else (m - lo) / (hi - lo)
+    return float(m.ravel()[0])
+
+
+def reference_time(w, x: np.ndarray, procs: int, disable_numba: bool, reps: int = 3):
+    """The unmodified reference (baseline/_ref) in a process pool, one clip per task,
+    after one warm-up clip per worker (numba JIT); median of ``reps`` timed runs."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    if not os.path.isdir(os.path.join(REF_PATH, "wavehop")):
+        return None
+    ctx = mp.get_context("spawn")
+    tasks = [(x[c], w["scales"], w["hop"], w["wavelet"], w["output"], w["norm"]) for c in range(x.shape[0])]
+    with ProcessPoolExecutor(procs, mp_context=ctx, initializer=_ref_worker_init,
+                             initargs=(REF_PATH, disable_numba)) as ex:
+        warm = [(x[0][:4000], w["scales"][:2], w["hop"], w["wavelet"], w["output"], w["norm"])] * procs
+        list(ex.map(_ref_clip, warm))
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            list(ex.map(_ref_clip, tasks))
+            ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def unmodified_reference(w, x: np.ndarray, procs: int):
+    """both reference backends (numba default, WAVEHOP_DISABLE_NUMBA=1)."""
+    out = {}
+    for name, dis in (("numba", False), ("numpy", True)):
+        try:
+            t = reference_time(w, x, procs, dis)
+        except Exception as e:  # noqa: BLE001
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:200]}
+            continue
+        if t is None:
+            return {"unavailable": "baseline/_ref not installed"}
+        out[name] = {"value": coeffs(w, x.shape[0]) / t, "unit": UNIT, "seconds": t}
+    vals = [v["value"] for v in out.values() if "value" in v]
+    return {"value": max(vals) if vals else None, "unit": UNIT, "cores": procs, "kind": "reference",
+            "backends": out,
+            "sample": f"{x.shape[0]} clips of {w['name']}: wavehop.cwth_strided (baseline/_ref, "
+                      f"unmodified) + float64 epilogue, ProcessPool x{procs}, one clip per task, "
+                      f"median of 3 after a per-worker warm-up; value = the faster backend"}
+
+
+def parity_check(w, got: np.ndarray, x: np.ndarray, clip_ids):
+    """Untimed check of sampled clips of the timed output against the oracle (f64).
+    Tolerance: per (clip, scale) row max|d| / max|ref row|
+    <= 1e-5; log1p absolute 1e-5; min-max absolute 1e-5 * max / (max - min) of the clip's
+    un-normalised values."""
+    from oracle import oracle as O
+
+    threads = len(os.sched_getaffinity(0))
+    ref = O.cwth_batch(x, w["scales"], w["hop"], wavelet=w["wavelet"], output=w["output"],
+                       norm=w["norm"], threads=threads)
+    errs, tols = [], []
+    for i in range(got.shape[0]):
+        g, r = got[i].astype(np.float64), ref[i]
+        if w["norm"] == "minmax":
+            raw = O.cwth_batch(x[i:i + 1], w["scales"], w["hop"], wavelet=w["wavelet"],
+                               output=w["output"], norm=None, threads=threads)[0]
+            tol = 1e-5 * raw.max() / (raw.max() - raw.min())
+            err = float(np.abs(g - r).max())
+        elif w["output"] == "log1p":
+            tol, err = 1e-5, float(np.abs(g - r).max())
+        else:
+            gm, rm = np.abs(g), np.abs(r)
+            if w["output"] == "complex":
+                gm, rm = got[i], ref[i]
+            rowmax = np.abs(rm).max(axis=-1, keepdims=True)
+            tol, err = 1e-5, float((np.abs(gm - rm) / np.where(rowmax > 0, rowmax, 1.0)).max())
+        errs.append(err)
+        tols.append(float(tol))
+    ok = all(e <= t for e, t in zip(errs, tols))
+    return {"clips": [int(c) for c in clip_ids], "max_err": errs, "tol": tols, "ok": bool(ok),
+            "shape_exact": list(got.shape[1:]) == [len(w["scales"]), -(-w["n"] // w["hop"])]}
+
+
+# ---------------------------------------------------------------------------------------
+# --impl reference
+# ---------------------------------------------------------------------------------------
+
 def run_reference(args, w):
-    """--impl reference: the reference's CPU path (oracle port) on the host cores."""
+    """The reference's CPU path on the host cores: the oracle port (all host threads, a
+    bounded sample of the workload per step); the unmodified reference package is timed
+    once beside it."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return 0
@@ -183,58 +344,80 @@ def run_reference(args, w):
     sample = min(args.ref_clips, w["clips"])
     x = make_inputs(w, sample, 0)
     for _ in range(max(args.warmup, 1)):
-        cpu_reference(w, x[: min(4, sample)], threads)
-    times = [cpu_reference(w, x, threads) for _ in range(args.steps)]
+        port_time(w, x[: min(4, sample)], threads)
+    times = [port_time(w, x, threads) for _ in range(args.steps)]
     t = sum(times)
     value = coeffs(w, sample) * args.steps / t
+    unmod = None if args.no_unmodified_ref else unmodified_reference(w, x[: min(sample, 2 * threads)], threads)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded MIMII stand-in, SURVEY.md §8d)",
-        # the same keys as the GPU arm's config; a step is `sample` clips (the whole per-GPU
-        # batch for c2) on the host cores
-        "config": {"workload": w["name"], "clips_per_gpu": sample, "n_samples": w["n"],
+        "config": {"workload": w["name"], "clips": sample, "n_samples": w["n"],
                    "scales": len(w["scales"]), "scale_range": [float(w["scales"][0]),
                                                               float(w["scales"][-1])],
                    "hop": w["hop"], "wavelet": w["wavelet"], "output": w["output"],
-                   "norm": w["norm"], "engine": "cpu-oracle-port", "parallelism": f"host threads x{threads}",
-                   "l2": "n/a (host)"},
+                   "norm": w["norm"], "engine": "cpu-oracle-port",
+                   "parallelism": f"host threads x{threads}", "l2": "n/a (host)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} clips of {w['name']} per step, oracle/wh_oracle.c "
-                                   f"folded f64 kernel (numba-equivalent), {threads} threads"},
+                         "sample": f"{sample} clips of {w['name']} per step (a bounded sample of "
+                                   f"the workload), oracle/wh_oracle.c folded f64 kernel "
+                                   f"(numba-equivalent) + the reference's epilogue, {threads} threads",
+                         "unmodified_reference": unmod},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ---------------------------------------------------------------------------------------
+# --impl ours
+# ---------------------------------------------------------------------------------------
+
 def run_ours(args, w):
     import torch
 
     world, rank, local = dist_setup()
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        print(json.dumps({"error": "no CUDA device"}), flush=True)
+        return 1
+    dev_index = local % ndev
+    shared_gpu = world > ndev
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        # one GPU per rank: NCCL (control only -- barrier and the max-over-ranks timing
+        # reduction; the data path has no collective).  More ranks than GPUs is a test
+        # mode (ranks share a device): gloo on host tensors.
+        if shared_gpu:
+            print(f"[bench] WARNING: {world} ranks on {ndev} GPU(s): ranks share devices "
+                  f"(test mode, gloo)", file=sys.stderr, flush=True)
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     import paper_2408_14302_b200 as wh
+    from paper_2408_14302_b200.shard import shard_range
 
     # shard: weak scaling keeps the per-rank batch; strong scaling splits the total
     if w["scaling"] == "weak":
         per_rank = args.clips or w["clips"]
         start = rank * per_rank
     else:
-        from paper_2408_14302_b200.shard import shard_range
-
         total = args.clips or w["clips"]
         start, stop = shard_range(total, world, rank)
         per_rank = stop - start
+    props = torch.cuda.get_device_properties(dev)
+    print(f"[bench] rank {rank}/{world} local {local} -> cuda:{dev_index} {props.name} "
+          f"(uuid {str(getattr(props, 'uuid', '?'))[:13]}) clips [{start}, {start + per_rank})",
+          file=sys.stderr, flush=True)
     xh = make_inputs(w, per_rank, start)
     params = wh.MorletParams()
     plan = wh.CwthPlan(w["scales"], params, w["hop"], w["n"], wavelet=w["wavelet"],
-                       output=w["output"], norm=w["norm"], max_clips=per_rank, device=local,
+                       output=w["output"], norm=w["norm"], max_clips=per_rank, device=dev_index,
                        engine=args.engine)
     x = torch.from_numpy(xh).to(dev)
     out_dtype = torch.complex64 if w["output"] == "complex" else torch.float32
@@ -248,7 +431,7 @@ def run_ours(args, w):
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
-    # ---- device-resident timed region -------------------------------------------------
+    # ---- device-resident timed region (L2 flushed before every step) -------------------
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             flush.zero_()
@@ -256,7 +439,7 @@ def run_ours(args, w):
     barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         clk.wait_first()
         barrier()
         n0 = len(clk.lines)
@@ -272,11 +455,25 @@ def run_ours(args, w):
         t0 = time.time()
         while len(clk.lines) < n0 + 4 and time.time() - t0 < 2.0:
             with torch.cuda.stream(stream):
-                for _ in range(8):
+                for _ in range(2):
                     flush.zero_()
                     plan.execute(x, out, stream=stream)
             torch.cuda.synchronize(dev)
-    dev_ms = sum(s.elapsed_time(e) for s, e in evs)
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    dev_ms = sum(step_ms)
+    # ---- steady state: the same steps back to back, no flush ----------------------------
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for _ in range(args.steps):
+            plan.execute(x, out, stream=stream)
+        b.record(stream)
+    barrier()
+    noflush_ms = a.elapsed_time(b) / args.steps
+    # keep the timed output (the last step) for the parity check
+    check_ids = sorted({0, per_rank // 2, per_rank - 1})
+    got = out[check_ids].cpu().numpy() if args.parity else None
     # ---- end-to-end through the public API with pinned host buffers ------------------
     e2e_ms = None
     if not args.no_e2e:
@@ -291,37 +488,28 @@ def run_ours(args, w):
             plan.execute_host(xnp, onp)
         e2e_ms = 1e3 * (time.perf_counter() - t0)
         barrier()
+        del xpin, opin
     # ---- reduce over ranks --------------------------------------------------------------
-    vals = torch.tensor([dev_ms, e2e_ms or 0.0], dtype=torch.float64, device=dev)
+    red = [dev_ms, e2e_ms or 0.0, noflush_ms]
     if world > 1:
-        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
-    dev_ms, e2e_ms_max = float(vals[0]), float(vals[1])
+        t = torch.tensor(red, dtype=torch.float64, device="cpu" if shared_gpu else dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        red = [float(v) for v in t.cpu()]
+        ranks = [None] * world
+        torch.distributed.all_gather_object(ranks, {"rank": rank, "device": dev_index,
+                                                    "clips": [start, start + per_rank],
+                                                    "ms_per_step": dev_ms / args.steps})
+    else:
+        ranks = [{"rank": 0, "device": dev_index, "clips": [start, start + per_rank],
+                  "ms_per_step": dev_ms / args.steps}]
+    dev_ms, e2e_ms_max, noflush_ms = red
     total_clips = per_rank * world if w["scaling"] == "weak" else (args.clips or w["clips"])
     value = coeffs(w, total_clips) * args.steps / (dev_ms / 1e3)
-    result = None
     if rank == 0:
         bf16, bf16_sus, hbm, peak_kind = peaks()
-        # main-kernel time: with min-max normalisation the plan also launches the
-        # reset/normalise kernels; time the main kernel alone through a norm=None plan
-        kern_ms = dev_ms / args.steps
-        if w["norm"] is not None:
-            plan2 = wh.CwthPlan(w["scales"], params, w["hop"], w["n"], wavelet=w["wavelet"],
-                                output=w["output"], norm=None, max_clips=per_rank, device=local,
-                                engine=args.engine)
-            with torch.cuda.stream(stream):
-                plan2.execute(x, out, stream=stream)
-                ks = []
-                for _ in range(min(args.steps, 5)):
-                    flush.zero_()
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                    plan2.execute(x, out, stream=stream)
-                    b.record(stream)
-                    ks.append((a, b))
-            torch.cuda.synchronize(dev)
-            kern_ms = statistics.median(a.elapsed_time(b) for a, b in ks)
-            plan2.close()
+        kern_ms = statistics.median(step_ms)
         flops = alg_flops(w, per_rank)
+        exec_flops = plan.mma_flops(per_rank)
         achieved = flops / (kern_ms / 1e3) / 1e12
         traffic = None
         tpath = os.path.join(REPO, "profiles", "traffic.json")
@@ -333,15 +521,20 @@ def run_ours(args, w):
         # The binding roof of the algorithm: algorithmic flops against the
         # measured bf16 tensor peak, or algorithmic bytes (input once + output once) against
         # the measured HBM copy bandwidth -- whichever lower bound on the kernel time is
-        # larger.  c2 (92 flop/B) sits below the ridge (1630e12 / 6547.5e9 = 249 flop/B): HBM.
+        # larger.  c5 (721 flop/B) is above the ridge: tensor; c2 (92 flop/B) below: HBM.
         alg_bytes = in_bytes + out_bytes
         t_tensor, t_hbm = flops / (bf16 * 1e12), alg_bytes / (hbm * 1e9)
         kern_s = kern_ms / 1e3
         common = {"traffic": traffic, "kernel": "k_umma" if plan.engine == "umma" else "k_simt",
-                  "kernel_ms": kern_ms, "alg_flops_per_launch": flops,
-                  "alg_bytes_per_launch": alg_bytes,
+                  "kernel_ms": kern_ms, "kernel_ms_noflush": noflush_ms,
+                  "kernel_note": "median CUDA-event step time on the launch stream; the step is "
+                                 "the engine kernel plus, for min-max plans, the per-clip key "
+                                 "reset (a few us); see profiles/ for the launch list shares",
+                  "alg_flops_per_launch": flops, "alg_bytes_per_launch": alg_bytes,
                   "tensor_view": {"achieved_tflops": achieved, "peak_tflops": bf16,
                                   "frac": achieved / bf16,
+                                  "executed_mma_tflops": (exec_flops / kern_s / 1e12) if exec_flops else None,
+                                  "executed_frac": (exec_flops / kern_s / 1e12 / bf16) if exec_flops else None,
                                   "note": "split-fp16 x3 products: executed MMA flops ~3x "
                                           "algorithmic (minus skipped tail cross terms) + K padding"},
                   "hbm_view": {"achieved_gbs": alg_bytes / kern_s / 1e9, "peak_gbs": hbm,
@@ -354,37 +547,46 @@ def run_ours(args, w):
         else:
             roofline = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                         "frac": achieved / bf16, **common}
-        cpu = None
+        # ---- CPU leg: baseline timings (N = 1) and the parity check of the timed output --
+        cpu, parity = None, None
+        threads = len(os.sched_getaffinity(0))
+        if args.parity:
+            parity = parity_check(w, got, xh[check_ids], [start + c for c in check_ids])
         if world == 1 and not args.no_cpu_baseline:
-            threads = len(os.sched_getaffinity(0))
             sample = min(per_rank, args.ref_clips)
             xs = xh[:sample]
-            cpu_reference(w, xs[:2], threads)  # warm-up
-            ts = [cpu_reference(w, xs, threads) for _ in range(3)]
+            port_time(w, xs[:2], threads)  # warm-up
+            ts = [port_time(w, xs, threads) for _ in range(3)]
             cpu = {"value": coeffs(w, sample) / statistics.median(ts), "unit": UNIT,
                    "cores": threads, "kind": "port",
                    "sample": f"{sample} clips of {w['name']} (the first clips of this workload), "
                              f"median of 3; oracle/wh_oracle.c folded f64 kernel with the "
                              f"reference's epilogue, {threads} threads"}
+            if not args.no_unmodified_ref:
+                cpu["unmodified_reference"] = unmodified_reference(w, xh[: min(sample, 2 * threads)], threads)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
             "scaling": w["scaling"], "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded MIMII stand-in, SURVEY.md §8d)",
-            "config": {"workload": w["name"], "clips_per_gpu": per_rank, "n_samples": w["n"],
-                       "scales": len(w["scales"]), "scale_range": [float(w["scales"][0]),
-                                                                  float(w["scales"][-1])],
+            "config": {"workload": w["name"], "clips_total": total_clips, "clips_per_gpu": per_rank,
+                       "n_samples": w["n"], "scales": len(w["scales"]),
+                       "scale_range": [float(w["scales"][0]), float(w["scales"][-1])],
                        "hop": w["hop"], "wavelet": w["wavelet"], "output": w["output"],
-                       "norm": w["norm"], "engine": plan.engine, "parallelism": f"clip-shard x{world}",
+                       "norm": w["norm"], "engine": plan.engine,
+                       "parallelism": f"clip-shard x{world}",
                        "l2": "flushed: 256 MiB device write before every timed step"},
+            "ms_per_step_noflush": noflush_ms,
             "e2e": {"value": (coeffs(w, total_clips) * args.e2e_steps / (e2e_ms_max / 1e3))
                     if e2e_ms is not None else None,
-                    "unit": UNIT, "h2d_bytes_per_step": int(in_bytes),
-                    "d2h_bytes_per_step": int(out_bytes),
+                    "unit": UNIT, "h2d_bytes_per_step": int(in_bytes * world if w["scaling"] == "weak" else 4.0 * total_clips * w["n"]),
+                    "d2h_bytes_per_step": int(out_bytes * world if w["scaling"] == "weak" else out_bytes / per_rank * total_clips),
                     "note": "CwthPlan.execute_host -> wh_execute_host: pinned H2D + kernels + "
                             "D2H of the full scalogram, host wall clock, max over ranks"},
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
+            "ranks": ranks,
             "gpu_launches": plan.launches(per_rank) * args.steps,
             "clocks": clk.summary(),
         }
@@ -399,23 +601,31 @@ def run_ours(args, w):
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2",
-                    help="c1..c5 or c4h{1,16,64,256,1024} (default c2 = BASELINE configs[1])")
+    ap.add_argument("--config", default=DEFAULT_CONFIG,
+                    help="c1..c5 or c4h{1,16,64,256,1024} (default c5, the metric's config)")
     ap.add_argument("--engine", choices=["auto", "simt", "umma"], default="auto")
     ap.add_argument("--clips", type=int, default=0, help="override clips per GPU (weak) / total (strong)")
-    ap.add_argument("--ref-clips", type=int, default=64, help="clips in the CPU-baseline sample")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--ref-clips", type=int, default=32, help="clips in the CPU-baseline sample")
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-unmodified-ref", action="store_true")
+    ap.add_argument("--no-parity", dest="parity", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     w = workload(args.config)
+    world_env = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         return run_reference(args, w)
+    if world_env is None and args.gpus > 1:
+        return spawn(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        print(f"error: --gpus {args.gpus} but WORLD_SIZE={world_env}", file=sys.stderr)
+        return 2
     return run_ours(args, w)
 
 

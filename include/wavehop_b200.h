@@ -104,6 +104,10 @@ int wh_plan_destroy(wh_plan *plan);
 int wh_plan_frames(const wh_plan *plan, int64_t *frames);
 int wh_plan_engine(const wh_plan *plan, int32_t *engine);
 int wh_plan_out_bytes(const wh_plan *plan, int64_t clips, int64_t *bytes);
+/* Tensor-core work one wh_execute of `clips` clips issues: the MMA flops the UMMA engine
+ * executes (split-fp16: three products minus the skipped tail cross terms, K padded to
+ * 64); 0 for the SIMT engine.  For the bench's roofline ("executed" vs algorithmic). */
+int wh_plan_mma_flops(const wh_plan *plan, int64_t clips, double *flops);
 /* Kernel launches one wh_execute issues (for the bench's gpu_launches claim). */
 int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches);
 /* Read back the device-built taps of one scale as fp32 (2L+1 values each of re/im,

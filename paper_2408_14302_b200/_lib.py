@@ -15,6 +15,9 @@ from .errors import DeviceError, EmptySignal, InvalidHop, InvalidScale
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libwavehop_b200.so")
+# tools only: WH_DIAG_LIB=1 loads the diagnostics build (build.py --diag)
+if os.environ.get("WH_DIAG_LIB") == "1":
+    LIB_PATH = os.path.join(HERE, "libwavehop_b200_diag.so")
 
 WH_OK = 0
 WH_E_INVALID_HOP = 1
@@ -48,6 +51,7 @@ SIGNATURES = {
     "wh_plan_engine": (ctypes.c_int, [_p, _pi32]),
     "wh_plan_out_bytes": (ctypes.c_int, [_p, _i64, _pi64]),
     "wh_plan_launches": (ctypes.c_int, [_p, _i64, _pi64]),
+    "wh_plan_mma_flops": (ctypes.c_int, [_p, _i64, ctypes.POINTER(ctypes.c_double)]),
     "wh_plan_taps": (ctypes.c_int, [_p, _i32, _p, _p, _i64, _pi64]),
     "wh_plan_profile": (ctypes.c_int, [_p, _i32, _p, _i32]),
     "wh_plan_trace": (ctypes.c_int, [_p, _i32, _p, _i32]),

@@ -83,11 +83,15 @@ int build_fold_bank(Plan &p) {
 
 // ---------------------------------------------------------------------------------------
 // Per-clip min-max (scalogram.py:77-83 affine map, without x255/round/uint8).
-__global__ void k_minmax_reset(uint32_t *mm, int64_t clips) {
+__global__ void k_minmax_reset(uint32_t *mm, uint32_t *arrive, uint32_t *abandon, int32_t ab_words, int64_t clips) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < clips) {
         mm[2 * i] = 0xffffffffu;  // min key
         mm[2 * i + 1] = 0u;       // max key
+        if (arrive) {
+            arrive[i] = 0u;
+            for (int w = 0; w < ab_words; ++w) abandon[i * ab_words + w] = 0u;
+        }
     }
 }
 
@@ -114,9 +118,8 @@ __global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip,
         base[i] = constant ? 0.0f : (base[i] - lo) * sc;
 }
 
-int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, cudaStream_t s) {
-    (void)p;
-    k_minmax_reset<<<(unsigned)((clips + 255) / 256), 256, 0, s>>>(mm, clips);
+int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, uint32_t *arrive, uint32_t *abandon, cudaStream_t s) {
+    k_minmax_reset<<<(unsigned)((clips + 255) / 256), 256, 0, s>>>(mm, arrive, abandon, p.ab_words, clips);
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }
@@ -201,7 +204,7 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
     cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
     cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow); cudaFree(p->d_tables);
-    cudaFree(p->d_minmax); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
+    cudaFree(p->d_minmax); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     cudaSetDevice(cur);
@@ -292,6 +295,14 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
             }
         }
     }
+    if (rc == WH_OK && norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA) {
+        // write-once min-max: per-clip unit arrivals + the bitmap of units left to the fix-up
+        const int64_t bits = (int64_t)((p->row_tiles + p->cg - 1) / p->cg) * (int64_t)p->passes.size() * p->cg;
+        p->ab_words = (int32_t)((bits + 31) / 32);
+        if (cudaMalloc(&p->d_arrive, sizeof(uint32_t) * max_clips) != cudaSuccess ||
+            cudaMalloc(&p->d_abandon, sizeof(uint32_t) * (size_t)max_clips * p->ab_words) != cudaSuccess)
+            rc = fail(WH_E_OOM, "cudaMalloc(min-max arrivals) failed");
+    }
     if (rc == WH_OK && (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
                         cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess))
         rc = fail(WH_E_CUDA, "cudaStreamCreate failed");
@@ -336,7 +347,22 @@ int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches) {
     if (!plan || !launches) return fail(WH_E_INVALID_ARG, "NULL argument");
     const Plan *p = reinterpret_cast<const Plan *>(plan);
     // engine + (min/max reset + normalise) or (reset + map parameters + uint8 map)
-    *launches = clips > 0 ? (1 + (p->norm == WH_NORM_MINMAX ? 2 : 0) + (is_render(*p) ? 3 : 0)) : 0;
+    // min-max: reset + (UMMA: the fix-up check | SIMT: the normalise pass)
+    const int mm = p->norm == WH_NORM_MINMAX ? 2 : 0;
+    *launches = clips > 0 ? (1 + mm + (is_render(*p) ? 3 : 0)) : 0;
+    return WH_OK;
+}
+
+int wh_plan_mma_flops(const wh_plan *plan, int64_t clips, double *flops) {
+    if (!plan || !flops) return fail(WH_E_INVALID_ARG, "NULL argument");
+    const Plan *p = reinterpret_cast<const Plan *>(plan);
+    *flops = 0.0;
+    if (p->engine != WH_ENGINE_UMMA || clips <= 0) return WH_OK;
+    // per tile (pair): every K-step tile issues 4 x (MMA1 N = nc + ncorr, MMA2 N = ncorr) of
+    // M = 128 * cg rows and K = 16
+    double per = 0.0;
+    for (const auto &t : p->tiles) per += 2.0 * 128.0 * p->cg * 64.0 * (double)(t.ncols + 2 * t.ncorr);
+    *flops = per * (double)clips * (double)((p->row_tiles + p->cg - 1) / p->cg);
     return WH_OK;
 }
 
@@ -368,16 +394,21 @@ int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im,
 
 // mm: this call's slice of the per-clip min/max keys; scratch: its slice of the float
 // values a render plan maps to uint8
+// arrive: this call's slice of the per-clip unit arrival counters (UMMA write-once min-max)
 static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev, cudaStream_t s,
-                        uint32_t *mm, float *scratch, void *rparams) {
+                        uint32_t *mm, uint32_t *arrive, uint32_t *abandon, float *scratch, void *rparams) {
     int rc = WH_OK;
     const bool render = is_render(*p);
     void *dst = render ? static_cast<void *>(scratch) : out_dev;
-    if (p->norm != WH_NORM_NONE) rc = minmax_reset(*p, clips, mm, s);
+    // the UMMA engine normalises min-max plans inside the kernel (write-once); the SIMT
+    // engine keeps the read-modify-write pass
+    const bool inkernel = p->norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA;
+    if (p->norm != WH_NORM_NONE) rc = minmax_reset(*p, clips, mm, inkernel ? arrive : nullptr, abandon, s);
     if (rc == WH_OK)
-        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm)
+        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm, inkernel ? arrive : nullptr,
+                                                         abandon)
                                            : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm);
-    if (rc == WH_OK && p->norm == WH_NORM_MINMAX) rc = minmax_apply(*p, clips, out_dev, mm, s);
+    if (rc == WH_OK && p->norm == WH_NORM_MINMAX && !inkernel) rc = minmax_apply(*p, clips, out_dev, mm, s);
     if (rc == WH_OK && render)
         rc = render_apply(scratch, clips, p->S, p->F, mm, rparams, p->norm == WH_NORM_RENDER_U8 ? 1 : 0,
                           static_cast<uint8_t *>(out_dev), s);
@@ -396,7 +427,8 @@ int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, v
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != p->device) WH_CUDA_TRY(cudaSetDevice(p->device));
-    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax, p->d_scratch, p->d_rparams);
+    const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax, p->d_arrive, p->d_abandon,
+                                p->d_scratch, p->d_rparams);
     if (prev != p->device) cudaSetDevice(prev);
     return rc;
 }
@@ -463,7 +495,8 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
             rc = fail(WH_E_CUDA, "H2D copy failed");
             break;
         }
-        rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0,
+        rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0, p->d_arrive ? p->d_arrive + c0 : nullptr,
+                          p->d_abandon ? p->d_abandon + (size_t)c0 * p->ab_words : nullptr,
                           p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr,
                           p->d_rparams ? static_cast<uint8_t *>(p->d_rparams) + (size_t)WH_RENDER_PARAM_BYTES * c0
                                        : nullptr);
@@ -480,6 +513,10 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
 
 int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n) {
     if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+#ifndef WH_DIAG
+    (void)enable; (void)counters; (void)n;
+    return fail(WH_E_UNSUPPORTED, "diagnostics need the WH_DIAG build (python -m paper_2408_14302_b200.build --diag)");
+#endif
     Plan *p = reinterpret_cast<Plan *>(plan);
     int prev = 0;
     cudaGetDevice(&prev);
@@ -496,7 +533,8 @@ int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n
         WH_CUDA_TRY(cudaMemset(p->d_prof, 0, sizeof(unsigned long long) * 20));
     }
     if (!enable) {
-        cudaFree(p->d_prof); cudaFree(p->d_trace);
+        // the profile counters only: the trace buffer belongs to wh_plan_trace
+        cudaFree(p->d_prof);
         p->d_prof = nullptr;
     }
     cudaSetDevice(prev);
@@ -505,6 +543,10 @@ int wh_plan_profile(wh_plan *plan, int32_t enable, uint64_t *counters, int32_t n
 
 int wh_plan_trace(wh_plan *plan, int32_t enable, int64_t *events, int32_t n) {
     if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
+#ifndef WH_DIAG
+    (void)enable; (void)events; (void)n;
+    return fail(WH_E_UNSUPPORTED, "diagnostics need the WH_DIAG build (python -m paper_2408_14302_b200.build --diag)");
+#endif
     Plan *p = reinterpret_cast<Plan *>(plan);
     int prev = 0;
     cudaGetDevice(&prev);

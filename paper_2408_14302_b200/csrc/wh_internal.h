@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -14,6 +15,20 @@ namespace wh {
 // diagnostics trace buffer (wh_plan_trace): CTA-0 timeline [16 events][32 units] of clock64,
 // then per CTA (up to 256) the %globaltimer (ns) at kernel entry and exit
 constexpr int WH_TRACE_N = 16 * 32 + 2 * 256;
+
+// Planner overrides (read once, at plan creation): select alternative but valid plan shapes
+// (the parity tests exercise them: WH_UMMA_HYBRID, _NO_RESIDENT, _CG1, _TAU, _NO_CONVREGS,
+// _G0_ALIGN, _PGROUPS, ...).  Never read at launch time.
+inline const char *plan_knob(const char *name) { return std::getenv(name); }
+// Diagnostics knobs (role switches, verbose plan dump): only in a -DWH_DIAG build.
+inline const char *diag_knob(const char *name) {
+#ifdef WH_DIAG
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 // Thread-local last-error message behind wh_last_error().
 void set_error(const std::string &msg);
@@ -111,6 +126,10 @@ struct Plan {
     int32_t simt_tf = 1;           // SIMT: frames per item tile
     bool doubled_v = false, no_2v = false;  // UMMA: rows of 2 lcm(hop, 64) samples (one pass)
     double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
+    bool no_convregs = false;      // UMMA planner override: converters without the register prefetch
+    bool force_fixup = false;      // UMMA planner override (tests): min-max units all to the fix-up kernel
+    int32_t pgroups_force = 0;     // UMMA planner override: pass groups per tile pair (0 = modelled)
+    int32_t dbg = 0;               // diagnostics role switches (WH_DIAG builds only)
     std::vector<int32_t> fexp;
     int32_t bstages = 2, win_bufs = 2;     // bstages: full-width tiles the ring holds (info)
     int64_t ring_bytes = 0;                // tap-tile ring capacity
@@ -127,6 +146,9 @@ struct Plan {
 
     // per-clip min/max (ordered-uint keys) for WH_NORM_MINMAX
     uint32_t *d_minmax = nullptr;  // [max_clips][2]
+    uint32_t *d_arrive = nullptr;  // UMMA write-once min-max: [max_clips] unit arrivals per clip
+    uint32_t *d_abandon = nullptr; // UMMA write-once min-max: [max_clips][ab_words] units left to the fix-up
+    int32_t ab_words = 0;
     float *d_scratch = nullptr;    // render plans: float values [max_clips][S][F] before the uint8 map
     void *d_rparams = nullptr;     // render plans: WH_RENDER_PARAM_BYTES per clip
 
@@ -147,10 +169,11 @@ int simt_prepare(Plan &p);
 int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm);
 int umma_supported(const Plan &p, std::string *why);
 int umma_prepare(Plan &p);
-int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm);
+int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
+                uint32_t *arrive, uint32_t *abandon);
 
 // epilogue helpers (wh_api.cu)
-int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, cudaStream_t s);
+int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, uint32_t *arrive, uint32_t *abandon, cudaStream_t s);
 constexpr int WH_RENDER_PARAM_BYTES = 24;  // per-matrix affine map of render_apply
 int render_apply(const float *values, int64_t clips, int64_t rows, int64_t cols, const uint32_t *mm, void *params,
                  int32_t flip, uint8_t *out, cudaStream_t s);

@@ -50,6 +50,17 @@ static constexpr int UM_SLOTS = 16;  // in-flight tap tiles (ring slots)
 static constexpr int UM_PF = 2;     // converters prefetch windows this many units ahead (L2)
 static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
 
+// Diagnostics (role switches, per-role wait counters, the CTA-0 timeline) exist only in a
+// build with -DWH_DIAG (paper_2408_14302_b200/build.py --diag); the product build compiles
+// them out of the kernel.
+#ifdef WH_DIAG
+static constexpr bool kDiag = true;
+#define WH_DBG(bit) ((A.dbg & (bit)) != 0)
+#else
+static constexpr bool kDiag = false;
+#define WH_DBG(bit) false
+#endif
+
 struct UmmaArgs {
     const float *x;
     int64_t ld_x, N, F, hop;
@@ -76,6 +87,11 @@ struct UmmaArgs {
     uint32_t tables_bytes;
     void *out;
     uint32_t *minmax;
+    uint32_t *arrive;               // write-once min-max: per-clip unit arrivals (nullptr: none)
+    uint32_t arrive_target;         // arrivals that complete a clip (CTAs x tile pairs x pass groups)
+    uint32_t *abandon;              // per clip ab_words words: units left to k_minmax_fixup
+    int32_t ab_words;               // bit ((tile pair * pgroups + pass group) * CG + CTA rank)
+    int32_t force_fixup;            // planner override (tests): every unit goes to the fix-up
     uint32_t ring_bytes, win_half_bytes;
     int32_t out_vec_ok;             // output base 16B aligned and F % 4 == 0
     int32_t out_vec8_ok;            // output base 32B aligned and F % 8 == 0 (256-bit stores)
@@ -143,7 +159,7 @@ __device__ __forceinline__ void prof_flush(const ProfAcc &pa, unsigned long long
 // diagnostics timeline (CTA 0 only): event e of unit u
 #define WH_TRACE(e, u)                                                                      \
     do {                                                                                    \
-        if (A.trace && blockIdx.x == 0 && (u) < 32 && lane == 0) A.trace[(e) * 32 + (u)] = clock64(); \
+        if (kDiag && A.trace && blockIdx.x == 0 && (u) < 32 && lane == 0) A.trace[(e) * 32 + (u)] = clock64(); \
     } while (0)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
@@ -416,11 +432,11 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
             const int sl0 = u0 / CP;
             float v[16], wr[16];
             tmem_ld16x2(tbase + u0, cbase - u0, v, wr);
-            if (!(A.dbg & 64)) {  // diagnostics: 64 = skip the re-zeroing (results invalid)
+            if (!WH_DBG(64)) {  // diagnostics: 64 = skip the re-zeroing (results invalid)
                 tmem_st16_zero(tbase + u0);
                 tmem_st16_zero(cbase - u0);
             }
-            if (A.dbg & 32) continue;  // diagnostics: 32 = skip the stores
+            if (WH_DBG(32)) continue;  // diagnostics: 32 = skip the stores
             if constexpr ((P == 1 || P == 2) && OUT != WH_OUT_COMPLEX64) if (A.rs == 1) {
                 // P = 1: one frame per lane -- transpose 4x4 blocks inside each lane quad (two
                 // xor-shuffle stages); P = 2: two frames per lane -- swap halves inside each
@@ -513,7 +529,7 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                             }
                         }
                     }
-                    if (A.dbg & 2048) {  // diagnostics: everything but the store instruction
+                    if (WH_DBG(2048)) {  // diagnostics: everything but the store instruction
                         if (t[0] + t[1] + t[2] + t[3] == 12345.678f) lmin = 0.0f;
                     } else if (sl0 + LPG * g + gi < ns) {
                         if (st4) {
@@ -658,6 +674,20 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
     }
 }
 
+// Per-window power-of-two scale 2^ex of the split-fp16 conversion: the window's max |x| lands
+// in [2^13, 2^14) (mx = m 2^E, m in [0.5, 1): ex = 14 - E).  Clamped to [-126, 126] so that
+// both 2^ex (converters) and 2^-ex (epilogue) are finite normal floats: a near-silent window
+// (max |x| < 2^-112) is scaled by 2^126 only -- its hi/lo parts are smaller than 2^13 but
+// still carry 22 bits relative to the window max down to |x| ~ 2^-150.  A window max of 0
+// (or not finite) gives ex = 0.
+__device__ __forceinline__ int window_exponent(float mx) {
+    if (!(mx > 0.0f) || !(mx <= 3.402823466e38f)) return 0;
+    int e = 0;
+    frexpf(mx, &e);
+    const int ex = 14 - e;
+    return ex > 126 ? 126 : (ex < -126 ? -126 : ex);
+}
+
 // window chunk c (8 consecutive samples) -> (row, chunk within the row) for cpr = panels * 8
 // chunks per row: row = (c * ceil(2^20 / cpr)) >> 20, exact for c < 131 k when cpr = 24 (checked
 // exhaustively; windows have < 5 k chunks), and for any c when cpr is a power of two
@@ -680,9 +710,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     __shared__ float red[UM_CONV_WARPS];
     __shared__ __align__(8) uint64_t stg_full, res_full, tab_full;
     __shared__ uint32_t tmem_base_sh;
+    __shared__ int s_decide;  // epilogue: CTA-uniform decision on the oldest pending unit
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
+    if (kDiag && A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
         A.trace[16 * 32 + 2 * blockIdx.x] = (long long)globaltimer_ns();
         if (blockIdx.x == 0) A.trace[14 * 32] = clock64();  // SM clock rate = cycles / ns
     }
@@ -846,7 +877,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     tc_fence_before();
     cta_pair_sync<CG>();
     tc_fence_after();
-    const bool pon = A.prof != nullptr;
+    const bool pon = kDiag && A.prof != nullptr;
     ProfAcc pa;
     pa.start();
 
@@ -902,7 +933,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     const long long t_issue = pon ? clock64() : 0;
                     if (elect_one()) {
                         s_vstart[slot] = v;
-                        if ((A.dbg & 128) && item != u0) {
+                        if (WH_DBG(128) && item != u0) {
                             mbar_arrive(&b_full[slot]);  // diagnostics: stale taps, no L2 traffic
                         } else {
                             mbar_expect_tx(&b_full[slot], bytes);
@@ -971,7 +1002,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         const uint32_t ah = a_hi16 + (tt.x & 0xffffu), al = ah + wh16;
                         const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
                         const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
-                        if (!(A.dbg & 4) && elect_one()) {
+                        if (!WH_DBG(4) && elect_one()) {
                             if (tt.w) {
 #pragma unroll
                                 for (uint32_t j = 0; j < 4; ++j) {
@@ -1032,7 +1063,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         // MMA issuer -- the leader's own barrier, directly from the peer CTA too
         auto window_ready = [&](uint32_t wb, uint32_t wcnt) {
             if (CG == 2 && !leader) {
-                if (A.dbg & 8) mbar_arrive_leader(&win_full[wb]);  // diagnostics: cluster-scope release
+                if (WH_DBG(8)) mbar_arrive_leader(&win_full[wb]);  // diagnostics: cluster-scope release
                 else mbar_arrive_leader_cta(&win_full[wb]);
             } else {
                 mbar_arrive(&win_full[wb]);
@@ -1110,11 +1141,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 mx = red[0];
 #pragma unroll
                 for (int i = 1; i < UM_CONV_WARPS; ++i) mx = fmaxf(mx, red[i]);
-                int ex = 0;
-                if (mx > 0.0f) {
-                    frexpf(mx, &ex);
-                    ex = 14 - ex;
-                }
+                const int ex = window_exponent(mx);
                 const float sc = ldexpf(1.0f, ex);
                 // split into hi/lo fp16 in registers (in place: 8 fp32 -> 4 hi + 4 lo words)
                 // while the window buffer is still busy; only the stores wait for it
@@ -1229,11 +1256,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mx = red[0];
 #pragma unroll
             for (int i = 1; i < UM_CONV_WARPS; ++i) mx = fmaxf(mx, red[i]);
-            int ex = 0;
-            if (mx > 0.0f) {
-                frexpf(mx, &ex);  // mx = m * 2^ex, m in [0.5, 1)
-                ex = 14 - ex;     // mx * 2^ex in [2^13, 2^14)
-            }
+            const int ex = window_exponent(mx);
             const float sc = ldexpf(1.0f, ex);
             // wait until the MMAs that read this window buffer win_bufs items ago are done
             if (ct == 0) WH_TRACE(5, wcnt);
@@ -1242,7 +1265,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             uint8_t *whi = win_base + (size_t)wb * 2 * WH;
             uint8_t *wlo = whi + WH;
 #pragma unroll 2
-            for (int c = ct; c < ((A.dbg & 2) ? 0 : chunks); c += UM_CONV_THREADS) {
+            for (int c = ct; c < (WH_DBG(2) ? 0 : chunks); c += UM_CONV_THREADS) {
                 int row, cc;
                     chunk_rc(A, c, row, cc);
                 const int panel = cc >> 3, c8 = cc & 7;
@@ -1279,10 +1302,106 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const int quad = warp & 3;          // TMEM lanes 32*quad .. 32*quad+31
         const int half = (warp - 2 - UM_CONV_WARPS) >> 2;  // which 16-column units
         const int m = quad * 32 + lane;     // row within the tile
+        const int et = (int)threadIdx.x - (64 + UM_CONV_THREADS);  // 0 .. 255
         const bool vec = A.out_vec_ok;
         uint32_t acnt = 0, ucnt = 0;
         float lmin = INFINITY, lmax = -INFINITY;
-        int64_t cur_b = -1;
+        // Write-once per-clip min-max (scalogram.py:77-83's affine map per clip): the units
+        // this CTA finished whose clip was still in flight elsewhere, oldest first -- a
+        // contiguous run of this CTA's unit sequence [pend_item, pend_item + pend*ustride).
+        // Their raw values sit in L2 (written one or two units ago); once every unit of the
+        // clip has arrived, the CTA re-reads its own tile region and overwrites it normalised,
+        // so the scalogram reaches HBM (close to) once, with no separate pass.
+        int64_t pend_item = u0;
+        int pend = 0;
+        auto clip_done = [&](int64_t b) {
+            uint32_t c;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(A.arrive + b) : "memory");
+            return c >= A.arrive_target;
+        };
+        auto normalise = [&](int64_t item) {
+            int64_t b, tile;
+            unit_tile(item, b, tile);
+            int pb, pe;
+            unit_passes(item, pb, pe);
+            const float lo = key2f(__ldcg(A.minmax + 2 * b)), hi = key2f(__ldcg(A.minmax + 2 * b + 1));
+            const bool constant = hi == lo;
+            const float sc = constant ? 0.0f : 1.0f / (hi - lo);
+            int64_t f0, f1;
+            if (A.rs > 1) {
+                f0 = (tile * 128 + A.rs - 1) / A.rs;
+                f1 = (tile * 128 + 128 + A.rs - 1) / A.rs;
+            } else {
+                f0 = tile * 128 * P;
+                f1 = f0 + 128 * P;
+            }
+            if (f1 > A.F) f1 = A.F;
+            const int len = (int)(f1 - f0);
+            if (len <= 0) return;
+            const bool v4 = vec && (f0 % 4) == 0;
+            const int nq = v4 ? (len + 3) / 4 : len;  // float4 groups (or scalars) per row
+            float *clip = reinterpret_cast<float *>(A.out) + b * (int64_t)A.S * A.F;
+            for (int p = pb; p < pe; ++p) {
+                const int4 pinfo = s_pass[p];
+                const int s0 = pinfo.z & 0xffff, ns = pinfo.z >> 16;
+                float *base = clip + (int64_t)s0 * A.F + f0;
+                for (int idx = et; idx < ns * nq; idx += 32 * UM_EPI_WARPS) {
+                    const int row = idx / nq, q = idx - row * nq;
+                    float *ptr = base + (int64_t)row * A.F;
+                    if (v4 && 4 * q + 4 <= len) {
+                        float4 v = __ldcg(reinterpret_cast<const float4 *>(ptr) + q);
+                        if (constant) {
+                            v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        } else {
+                            v.x = (v.x - lo) * sc; v.y = (v.y - lo) * sc; v.z = (v.z - lo) * sc; v.w = (v.w - lo) * sc;
+                        }
+                        st_na(reinterpret_cast<float4 *>(ptr) + q, v);
+                    } else {
+                        const int j0 = v4 ? 4 * q : q, j1 = v4 ? (4 * q + 4 < len ? 4 * q + 4 : len) : q + 1;
+                        for (int j = j0; j < j1; ++j) st_na(ptr + j, constant ? 0.0f : (__ldcg(ptr + j) - lo) * sc);
+                    }
+                }
+            }
+        };
+        // Normalise the finished units whose clips are complete.  The decision for the oldest
+        // pending unit is CTA-uniform (epilogue thread 0 decides, a named barrier publishes
+        // it): done -> normalise it here; still running after a bounded wait (only when more
+        // than `keep` units are pending, or at the end) -> hand it to the fix-up kernel
+        // (k_minmax_fixup), which normalises abandoned units after this launch.  No CTA ever
+        // waits unboundedly on another, so concurrent launches cannot deadlock.
+        auto decide = [&](int64_t b, bool may_wait) -> int {
+            if (et == 0) {
+                int st = clip_done(b) ? 1 : 0;
+                if (!st && may_wait) {
+                    const unsigned long long t0 = globaltimer_ns();
+                    while (!(st = clip_done(b)) && globaltimer_ns() - t0 < 200000ull) __nanosleep(512);
+                    if (!st) st = 2;
+                }
+                s_decide = st;
+            }
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * UM_EPI_WARPS) : "memory");
+            const int st = s_decide;
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * UM_EPI_WARPS) : "memory");
+            return st;
+        };
+        auto drain = [&](int keep) {
+            while (pend > 0) {
+                int64_t b, tile;
+                unit_tile(pend_item, b, tile);
+                const int st = A.force_fixup ? 2 : decide(b, pend > keep);
+                if (st == 0) break;
+                if (st == 1) {
+                    normalise(pend_item);
+                } else if (et == 0) {
+                    // abandoned: flag (tile pair, pass group, CTA) in the clip's bitmap
+                    const uint32_t v = (uint32_t)pend_item / pg32, bit =
+                        (((v - (uint32_t)b * tpu32) * pg32 + ((uint32_t)pend_item - v * pg32)) * CG) + rank;
+                    atomicOr(A.abandon + b * A.ab_words + (bit >> 5), 1u << (bit & 31));
+                }
+                pend_item += ustride;
+                --pend;
+            }
+        };
         for (int64_t item = u0; item < n_units; item += ustride, ++ucnt) {
             int64_t b, tile;
             unit_tile(item, b, tile);
@@ -1291,22 +1410,6 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             const int64_t frame0 = A.rs > 1 ? mrow / A.rs : mrow * P;
             const int64_t rem_frames = (A.rs > 1 && mrow % A.rs) ? 0 : A.F - frame0;
             const int nvalid = rem_frames <= 0 ? 0 : (rem_frames >= P ? P : (int)rem_frames);
-            if (A.minmax && b != cur_b) {
-                if (cur_b >= 0) {
-#pragma unroll
-                    for (int off = 16; off >= 1; off >>= 1) {
-                        lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
-                        lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-                    }
-                    if (lane == 0 && lmin <= lmax) {
-                        atomicMin(A.minmax + 2 * cur_b, f2key(lmin));
-                        atomicMax(A.minmax + 2 * cur_b + 1, f2key(lmax));
-                    }
-                }
-                lmin = INFINITY;
-                lmax = -INFINITY;
-                cur_b = b;
-            }
             int pb, pe;
             unit_passes(item, pb, pe);
             for (int p = pb; p < pe; ++p, ++acnt) {
@@ -1322,7 +1425,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 // from cbase - u0 in reverse order
                 const uint32_t cbase = tbase + 2u * (uint32_t)pinfo.w - 16u;
                 const int s0 = pinfo.z & 0xffff, ns = pinfo.z >> 16;
-                if (!(A.dbg & 1)) switch (A.output) {
+                if (!WH_DBG(1)) switch (A.output) {
                     case WH_OUT_COMPLEX64:
                         epi_pass<CC, P, WH_OUT_COMPLEX64>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
@@ -1351,18 +1454,34 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     else mbar_arrive(&acc_empty[ab]);
                 }
             }
-        }
-        if (A.minmax && cur_b >= 0) {
+            if (A.minmax) {
+                // this unit's min / max into the clip's keys (order-independent atomics)
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
-                lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-            }
-            if (lane == 0 && lmin <= lmax) {
-                atomicMin(A.minmax + 2 * cur_b, f2key(lmin));
-                atomicMax(A.minmax + 2 * cur_b + 1, f2key(lmax));
+                for (int off = 16; off >= 1; off >>= 1) {
+                    lmin = fminf(lmin, __shfl_xor_sync(0xffffffffu, lmin, off));
+                    lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
+                }
+                if (lane == 0 && lmin <= lmax) {
+                    atomicMin(A.minmax + 2 * b, f2key(lmin));
+                    atomicMax(A.minmax + 2 * b + 1, f2key(lmax));
+                }
+                lmin = INFINITY;
+                lmax = -INFINITY;
+                if (A.arrive) {
+                    // all epilogue warps' stores and key atomics of this unit are done: one
+                    // arrival per CTA and unit on the clip's counter (release at GPU scope)
+                    if (lane == 0) __threadfence();
+                    asm volatile("bar.sync 2, %0;" ::"r"(32 * UM_EPI_WARPS) : "memory");
+                    if (et == 0) {
+                        __threadfence();
+                        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.arrive + b) : "memory");
+                    }
+                    ++pend;
+                    drain(2);  // at most 2 units behind (a bounded L2 footprint)
+                }
             }
         }
+        if (A.arrive) drain(0);
     }
     if (pon && lane == 0) {
         const int role = warp == 0 ? PR_PROD : warp == 1 ? (leader ? PR_MMA : PR_RELAY) : warp < 2 + UM_CONV_WARPS ? PR_CONV : PR_EPI;
@@ -1370,7 +1489,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     }
     tc_fence_before();
     cta_pair_sync<CG>();
-    if (A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
+    if (kDiag && A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
         A.trace[16 * 32 + 2 * blockIdx.x + 1] = (long long)globaltimer_ns();
         if (blockIdx.x == 0) A.trace[14 * 32 + 1] = clock64();
     }
@@ -1381,6 +1500,57 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
         else
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ---- write-once min-max: fix-up of abandoned units ---------------------------------------
+// k_umma normalises every unit of a min-max plan itself once the unit's clip is complete; a
+// unit whose clip did not complete within a bounded wait (another kernel holding SMs, a
+// straggler at the very end) is flagged in its clip's bitmap instead.  This kernel, launched
+// right after k_umma on the same stream, normalises exactly the flagged regions (normally
+// none: every block reads its clips' bitmap words and exits).
+struct FixupArgs {
+    float *out;
+    const uint32_t *minmax, *abandon;
+    const int4 *passes;       // packed pass table (x, y = groups, z = s0 | ns << 16, w = cols)
+    int64_t clips, F;
+    int32_t S, P, rs, cg, tpu, pgroups, ppu, n_passes, ab_words, vec;
+};
+
+__global__ void k_minmax_fixup(const FixupArgs a) {
+    for (int64_t b = blockIdx.x; b < a.clips; b += gridDim.x) {
+        const float lo = key2f(a.minmax[2 * b]), hi = key2f(a.minmax[2 * b + 1]);
+        const bool constant = hi == lo;
+        const float sc = constant ? 0.0f : 1.0f / (hi - lo);
+        float *clip = a.out + b * (int64_t)a.S * a.F;
+        for (int w = 0; w < a.ab_words; ++w) {
+            uint32_t bits = a.abandon[b * a.ab_words + w];
+            while (bits) {
+                const int bit = 32 * w + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int rank = bit % a.cg, pg = (bit / a.cg) % a.pgroups, tp = bit / a.cg / a.pgroups;
+                const int64_t tile = (int64_t)a.cg * tp + rank;
+                int64_t f0, f1;
+                if (a.rs > 1) {
+                    f0 = (tile * 128 + a.rs - 1) / a.rs;
+                    f1 = (tile * 128 + 128 + a.rs - 1) / a.rs;
+                } else {
+                    f0 = tile * 128 * a.P;
+                    f1 = f0 + 128 * a.P;
+                }
+                if (f1 > a.F) f1 = a.F;
+                const int len = (int)(f1 - f0);
+                const int p0 = pg * a.ppu, p1 = p0 + a.ppu < a.n_passes ? p0 + a.ppu : a.n_passes;
+                for (int p = p0; p < p1 && len > 0; ++p) {
+                    const int s0 = a.passes[p].z & 0xffff, ns = a.passes[p].z >> 16;
+                    for (int idx = threadIdx.x; idx < ns * len; idx += blockDim.x) {
+                        const int row = idx / len, j = idx - row * len;
+                        float *ptr = clip + (int64_t)(s0 + row) * a.F + f0 + j;
+                        *ptr = constant ? 0.0f : (*ptr - lo) * sc;
+                    }
+                }
+            }
+        }
     }
 }
 
@@ -1547,6 +1717,10 @@ int umma_prepare(Plan &p) {
     return rc;
 }
 static int umma_prepare_impl(Plan &p) {
+    p.no_convregs = plan_knob("WH_UMMA_NO_CONVREGS") != nullptr;
+    p.force_fixup = plan_knob("WH_UMMA_MINMAX_FIXUP") != nullptr;
+    if (const char *e = plan_knob("WH_UMMA_PGROUPS")) p.pgroups_force = std::atoi(e);
+    if (const char *d = diag_knob("WH_UMMA_DBG")) p.dbg = std::atoi(d);
     // hop | 64: rows of 64 samples, P = 64/hop frames (phases) per row; hop = 64..256 (multiple
     // of 64): one frame per row of hop samples; hop = 256*RS: rows of 256 samples of which
     // every RS-th is a frame (the other rows are computed and dropped: RS x the tensor work,
@@ -1559,7 +1733,7 @@ static int umma_prepare_impl(Plan &p) {
         // be double-buffered: measured c4 hop 256 / 1024 274 / 260 us with rows of 256, 227 / 226
         // with rows of 128 (2x the rows computed, windows half the size), 286 with rows of 64.
         int64_t R = 128;
-        if (const char *r = std::getenv("WH_UMMA_ROW"))  // diagnostics: rows of 256 where hop % 256 == 0
+        if (const char *r = plan_knob("WH_UMMA_ROW"))  // diagnostics: rows of 256 where hop % 256 == 0
             if (std::atoi(r) == 256 && H % 256 == 0) R = 256;
         if (H >= 256 && H % R == 0 && (H > 256 || R < 256)) {
             p.rs = (int32_t)(H / R);
@@ -1575,10 +1749,10 @@ static int umma_prepare_impl(Plan &p) {
         // beside two windows); with more columns the second pass re-reads A (c2: 65 -> 110 us)
         const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
         p.doubled_v = p.rs == 1 && 2 * p.V <= 256 && 2 * (p.V / H) * cc * (int64_t)p.S <= 128 && !p.no_2v &&
-                      std::getenv("WH_UMMA_V") == nullptr && std::getenv("WH_UMMA_NO_2V") == nullptr;
+                      plan_knob("WH_UMMA_V") == nullptr && plan_knob("WH_UMMA_NO_2V") == nullptr;
         if (p.doubled_v) p.V *= 2;
     }
-    if (const char *v = std::getenv("WH_UMMA_V")) {  // experiment: more phases per row
+    if (const char *v = plan_knob("WH_UMMA_V")) {  // experiment: more phases per row
         const int vv = std::atoi(v);
         if (vv >= p.V && vv % 64 == 0 && vv % H == 0 && p.rs == 1) p.V = vv;
     }
@@ -1601,7 +1775,7 @@ static int umma_prepare_impl(Plan &p) {
 
     const int CP = p.Cc * p.P;
     int tau_log2 = 8;  // correction-term threshold tau = 2^-8 (WH_UMMA_TAU=0: never skip)
-    if (const char *t = std::getenv("WH_UMMA_TAU")) tau_log2 = std::atoi(t);
+    if (const char *t = plan_knob("WH_UMMA_TAU")) tau_log2 = std::atoi(t);
     // TMEM: 512 columns = 2 accumulator buffers x (128 main + 128 correction) columns, so a
     // pass covers at most 128 columns and the epilogue of pass n overlaps the MMAs of n+1.
     const int max_cols = 128;
@@ -1694,7 +1868,7 @@ static int umma_prepare_impl(Plan &p) {
                 best_cost = c;
             }
         }
-        if (const char *g = std::getenv("WH_UMMA_G0_ALIGN")) {  // diagnostics: force an alignment
+        if (const char *g = plan_knob("WH_UMMA_G0_ALIGN")) {  // diagnostics: force an alignment
             const int64_t al = std::max(4, std::atoi(g)) / 4 * 4;
             best = (p.Lmax + al - 1) / al * al;
         }
@@ -1708,7 +1882,7 @@ static int umma_prepare_impl(Plan &p) {
     const int64_t win = 2LL * p.panels * p.win_rows * 128;
     int64_t byte_off = 0;
     // CTA pairs (tcgen05 cta_group::2, M = 256): each CTA stages half of every tap tile
-    p.cg = (p.sms % 2 == 0 && std::getenv("WH_UMMA_CG1") == nullptr) ? 2 : 1;
+    p.cg = (p.sms % 2 == 0 && plan_knob("WH_UMMA_CG1") == nullptr) ? 2 : 1;
     // Group consecutive tiles of a pass into one bulk copy of up to group_target bytes per
     // CTA: a copy costs ~250 issue cycles whatever its size (tools/probe_bulk.cu), so small
     // tiles must travel together.  Bank layout per group: [CTA-0 blocks][CTA-1 blocks].
@@ -1736,7 +1910,7 @@ static int umma_prepare_impl(Plan &p) {
     // than the hidden conversion; default is one window, all resident).  (3) otherwise
     // stream everything.
     const int64_t n_tiles = (int64_t)p.tiles.size();
-    const bool allow_res = std::getenv("WH_UMMA_NO_RESIDENT") == nullptr;
+    const bool allow_res = plan_knob("WH_UMMA_NO_RESIDENT") == nullptr;
     int64_t t_split = 0;  // tiles [0, t_split) resident
     int hybrid = 0;
     int64_t stream_target = 0;
@@ -1744,10 +1918,10 @@ static int umma_prepare_impl(Plan &p) {
         t_split = n_tiles;
     } else if (allow_res && bank_cta + win <= budget0) {
         t_split = n_tiles;
-        if (std::getenv("WH_UMMA_HYBRID") != nullptr) {
+        if (plan_knob("WH_UMMA_HYBRID") != nullptr) {
             stream_target = 8 * 1024;
             int64_t hyb_ring = 32 * 1024;
-            if (const char *r = std::getenv("WH_UMMA_HYB_RING_KB")) hyb_ring = std::max(8, std::atoi(r)) * 1024;
+            if (const char *r = plan_knob("WH_UMMA_HYB_RING_KB")) hyb_ring = std::max(8, std::atoi(r)) * 1024;
             const int64_t res_limit = budget0 - 2 * win - hyb_ring;
             int64_t acc = 0, t = 0;
             while (t < n_tiles && acc + tile_bytes(p.tiles[t]) <= res_limit) acc += tile_bytes(p.tiles[t++]);
@@ -1767,7 +1941,7 @@ static int umma_prepare_impl(Plan &p) {
     const int64_t two_win_groups = std::min<int64_t>(48 * 1024, (budget0 - 2 * win) / 3 / 1024 * 1024);
     const int64_t group_target = p.resident ? 48 * 1024 : (n_tiles >= 64 ? 48 * 1024 : std::max<int64_t>(16 * 1024, two_win_groups));
     int64_t group_target_env = 0;
-    if (const char *g = std::getenv("WH_UMMA_GROUP_KB")) group_target_env = std::max(1, std::atoi(g)) * 1024;
+    if (const char *g = plan_knob("WH_UMMA_GROUP_KB")) group_target_env = std::max(1, std::atoi(g)) * 1024;
     p.groups_u.clear();
     int64_t max_group = 0, res_bytes = 0;
     int n_stream = 0;
@@ -1836,7 +2010,7 @@ static int umma_prepare_impl(Plan &p) {
         const int opts_stg[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
         const int opts_regs[4][2] = {{2, 0}, {1, 0}, {2, 1}, {1, 1}};
         const int (*opts_r)[2] = regs_ok ? opts_regs : opts_stg;
-        const int r0 = std::getenv("WH_UMMA_WIN1") ? (regs_ok ? 1 : 2) : 0;  // diagnostics: one window
+        const int r0 = plan_knob("WH_UMMA_WIN1") ? (regs_ok ? 1 : 2) : 0;  // diagnostics: one window
         for (int i = r0; i < 4; ++i) {
             const int *o = opts_r[i];
             if ((int64_t)(o[0] + o[1]) * win + ring <= budget) {
@@ -1853,11 +2027,11 @@ static int umma_prepare_impl(Plan &p) {
         use_stg = 0;
         ring = res_bytes + rest;
     } else {
-        const int prefer_single = n_tiles >= 64 && std::getenv("WH_UMMA_PREFER_DOUBLE") == nullptr;
+        const int prefer_single = n_tiles >= 64 && plan_knob("WH_UMMA_PREFER_DOUBLE") == nullptr;
         const int opts_a[4][2] = {{2, 0}, {2, 1}, {1, 1}, {1, 0}};
         const int opts_b[4][2] = {{1, 1}, {2, 1}, {1, 0}, {2, 0}};
         const int (*opts)[2] = prefer_single ? opts_b : opts_a;
-        const char *force = std::getenv("WH_UMMA_SMEM_OPT");  // diagnostics: force an option
+        const char *force = plan_knob("WH_UMMA_SMEM_OPT");  // diagnostics: force an option
         const int ostart = force ? std::atoi(force) : 0;
         for (int i = ostart; i < 4; ++i) {
             const int64_t fixed = (int64_t)(opts[i][0] + opts[i][1]) * win;
@@ -1967,7 +2141,7 @@ static int umma_prepare_impl(Plan &p) {
             p.grid_ctas = std::min(p.sms, 2 * clusters);
         (void)cudaGetLastError();
     }
-    if (std::getenv("WH_UMMA_VERBOSE")) {  // diagnostics: the plan's shape
+    if (diag_knob("WH_UMMA_VERBOSE")) {  // diagnostics: the plan's shape
         int64_t ncorr = 0, ncols = 0;
         for (auto &t : p.tiles) ncols += t.ncols, ncorr += t.ncorr;
         std::fprintf(stderr,
@@ -1981,7 +2155,8 @@ static int umma_prepare_impl(Plan &p) {
     return WH_OK;
 }
 
-int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm) {
+int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
+                uint32_t *arrive, uint32_t *abandon) {
     UmmaArgs a{};
     a.x = x; a.ld_x = ld_x; a.N = p.N; a.F = p.F; a.hop = p.hop;
     a.row_tiles = p.row_tiles; a.V = p.V; a.P = p.P; a.Cc = p.Cc; a.panels = p.panels; a.rs = p.rs;
@@ -1996,19 +2171,26 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.cpr = p.panels * 8;
     a.pf = p.V >= 256 ? 1 : 0;
     a.cpr_magic = ((1 << 20) + a.cpr - 1) / a.cpr;
-    a.conv_regs = (!p.use_stg && std::getenv("WH_UMMA_NO_CONVREGS") == nullptr) ? 1 : 0;
+    a.conv_regs = (!p.use_stg && !p.no_convregs) ? 1 : 0;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.tables = p.d_tables; a.tables_bytes = (uint32_t)p.tables_bytes;
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
     a.out = out;
     a.minmax = p.norm != WH_NORM_NONE ? mm : nullptr;
+    // write-once min-max: the kernel normalises each clip itself (arrival counters live right
+    // after this launch's keys: the caller's slice of d_minmax is [clips][2], d_arrive the
+    // matching [clips] slice)
+    a.arrive = p.norm == WH_NORM_MINMAX ? arrive : nullptr;
+    a.abandon = a.arrive ? abandon : nullptr;
+    a.ab_words = p.ab_words;
+    a.force_fixup = p.force_fixup ? 1 : 0;
     a.clips = clips;
     a.ring_bytes = (uint32_t)p.ring_bytes;
     a.win_half_bytes = (uint32_t)p.panels * (uint32_t)p.win_rows * 128u;
     a.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (p.F % 4 == 0);
     a.out_vec8_ok = ((reinterpret_cast<uintptr_t>(out) & 31) == 0) && (p.F % 8 == 0);
     a.prof = p.d_prof;
-    a.dbg = std::getenv("WH_UMMA_DBG") ? std::atoi(std::getenv("WH_UMMA_DBG")) : 0;
+    a.dbg = p.dbg;
     a.trace = p.d_trace;
     // Split each tile pair's passes into G groups (separate units) when there are too few
     // units to fill the CTA pairs evenly (c3: 80 tile pairs on 74 CTA pairs): minimise
@@ -2041,10 +2223,11 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
             best_fill = fill;
         }
     }
-    if (const char *e = std::getenv("WH_UMMA_PGROUPS")) G = std::max(1, std::min(n_passes, std::atoi(e)));
+    if (p.pgroups_force > 0) G = std::max(1, std::min(n_passes, p.pgroups_force));
     a.ppu = (n_passes + G - 1) / G;
     a.pgroups = (n_passes + a.ppu - 1) / a.ppu;
     const int64_t units = tile_units * a.pgroups;
+    a.arrive_target = (uint32_t)(p.cg * ((p.row_tiles + p.cg - 1) / p.cg) * a.pgroups);
     if (units >= ((int64_t)1 << 31)) return fail(WH_E_INVALID_ARG, "UMMA engine: too many clips for one launch");
     int64_t grid = std::min<int64_t>(units * p.cg, p.grid_ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
@@ -2063,6 +2246,18 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     cfg.numAttrs = 1;
     WH_CUDA_TRY(cudaLaunchKernelEx(&cfg, umma_kernel(p.Cc, p.P, p.cg), a));
     WH_CUDA_TRY(cudaGetLastError());
+    if (a.arrive) {
+        FixupArgs f{};
+        f.out = static_cast<float *>(out);
+        f.minmax = mm;
+        f.abandon = abandon;
+        f.passes = reinterpret_cast<const int4 *>(p.d_tables);  // the packed pass table leads the blob
+        f.clips = clips; f.F = p.F; f.S = p.S; f.P = p.P; f.rs = p.rs; f.cg = p.cg;
+        f.tpu = (int32_t)((p.row_tiles + p.cg - 1) / p.cg); f.pgroups = a.pgroups; f.ppu = a.ppu;
+        f.n_passes = n_passes; f.ab_words = p.ab_words;
+        k_minmax_fixup<<<(unsigned)std::min<int64_t>(clips, 4 * p.sms), 256, 0, s>>>(f);
+        WH_CUDA_TRY(cudaGetLastError());
+    }
     return WH_OK;
 }
 

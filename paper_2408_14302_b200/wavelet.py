@@ -200,6 +200,12 @@ class CwthPlan:
         _lib.check(_lib.load().wh_plan_launches(self._h, int(clips), ctypes.byref(n)))
         return n.value
 
+    def mma_flops(self, clips: int) -> float:
+        """Tensor-core flops one execute() of ``clips`` clips issues (0 for the SIMT engine)."""
+        f = ctypes.c_double()
+        _lib.check(_lib.load().wh_plan_mma_flops(self._h, int(clips), ctypes.byref(f)))
+        return f.value
+
     def taps(self, index: int) -> np.ndarray:
         """Device-built taps of scale ``index`` as complex64 (2L+1 values)."""
         L = half_width(self.scales[index], self.params)

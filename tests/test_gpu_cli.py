@@ -9,6 +9,7 @@ from conftest import row_rel_err
 from oracle import oracle as O
 import paper_2408_14302_b200 as wh
 from paper_2408_14302_b200 import cli, scalogram as S, wavio
+import signals
 
 pytestmark = pytest.mark.gpu
 
@@ -20,14 +21,16 @@ def _grid(rate, n_scales=24, fmin=50.0, fmax=None):
 @pytest.mark.parametrize("mode", ["strided", "decimate", "full"])
 def test_transform_command(tmp_path, mode):
     out = tmp_path / "a.scg1"
-    argv = ["transform", "white_noise:seed=3", "--out", str(out), "--length", "8000", "--rate", "8000",
+    sig = signals.white_noise(8000, 8000.0, seed=3)
+    wavio.write_wav(sig, tmp_path / "in.wav", encoding="float32")
+    argv = ["transform", str(tmp_path / "in.wav"), "--out", str(out),
             "--mode", mode, "--hop", "16", "--scales", "24", "--fmin", "50",
             "--csv", str(tmp_path / "a.csv"), "--pgm", str(tmp_path / "a.pgm")]
     if mode == "decimate":
         argv.append("--anti-alias")
     assert cli.run_cli(argv) == 0
     m = S.read_matrix_bin(out)
-    sig = wavio.synthesize(wavio.SynthSpec("white_noise", 8000, 8000.0, seed=3))
+    sig = wavio.read_wav(tmp_path / "in.wav")  # float32 on disk: the samples the CLI saw
     rate = 8000.0 / 16 if mode == "decimate" else 8000.0
     grid = _grid(rate)
     np.testing.assert_array_equal(m.scale_grid.scales, grid.scales)

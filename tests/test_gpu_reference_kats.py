@@ -9,7 +9,8 @@ import pytest
 
 from conftest import max_rel_err
 import paper_2408_14302_b200 as wh
-from paper_2408_14302_b200 import wavio
+from paper_2408_14302_b200 import wavio  # noqa: F401
+import signals
 
 pytestmark = pytest.mark.gpu
 
@@ -84,7 +85,7 @@ def test_decimate_equals_transform_of_decimated_signal():
 
 def test_decimate_sine_peaks_at_expected_row():
     # test_wavelet.py:305-313
-    sig = wavio.synthesize(wavio.SynthSpec("sine", 8192, 16_000.0, frequency=1000.0))
+    sig = signals.sine(8192, 16_000.0, 1000.0)
     grid = wh.make_scale_grid(100.0, 3500.0, 32, 8000.0, PARAMS)
     out = wh.cwth_decimate(sig, grid, PARAMS, 2)
     power = np.mean(np.abs(out.values) ** 2, axis=1)
@@ -96,7 +97,7 @@ def test_decimate_sine_peaks_at_expected_row():
 
 def test_decimate_distinct_from_strided():
     # test_wavelet.py:315-323: 6 kHz folds to DC after decimation by 128
-    sig = wavio.synthesize(wavio.SynthSpec("sine", 16_384, 16_000.0, frequency=6000.0))
+    sig = signals.sine(16_384, 16_000.0, 6000.0)
     grid = wh.make_scale_grid(10.0, 50.0, 6, 16_000.0, PARAMS)
     strided = wh.cwth_strided(sig, grid, PARAMS, 128)
     decimated = wh.cwth_decimate(sig, grid, PARAMS, 128)
@@ -124,7 +125,7 @@ def test_linear_combination(transform):
 def test_peak_magnitude_tracks_inverse_sqrt_scale():
     # test_wavelet.py:349-357 (same 1e-6 as the reference: x = 1 is exact in fp16)
     n = 4096
-    sig = wavio.synthesize(wavio.SynthSpec("impulse", n, 16_000.0, position=n // 2))
+    sig = signals.impulse(n, 16_000.0, n // 2)
     grid = wh.make_scale_grid(500.0, 6000.0, 16, 16_000.0, PARAMS)
     peaks = np.abs(wh.cwt_fft(sig, grid, PARAMS).values).max(axis=1)
     expected = (math.pi * PARAMS.bandwidth) ** -0.5 / np.sqrt(grid.scales)

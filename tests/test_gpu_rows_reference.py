@@ -10,6 +10,7 @@ import pytest
 
 import paper_2408_14302_b200 as wh
 from paper_2408_14302_b200 import cli, scalogram as S, wavio
+import signals
 from paper_2408_14302_b200.bench import BenchReport, bench_single, extrapolate_dataset, reports_to_jsonl
 
 pytestmark = pytest.mark.gpu
@@ -53,11 +54,11 @@ def test_decimate_composition_and_invalid_hop():
 
 
 def test_anti_alias_suppresses_folding_and_passes_low_frequencies():
-    hi = wavio.synthesize(wavio.SynthSpec("sine", 8000, 16_000, frequency=3600.0))
+    hi = signals.sine(8000, 16_000, 3600.0)
     plain, filt = wh.decimate(hi, 4).samples, wh.decimate(hi, 4, anti_alias=True).samples
     assert len(filt) == len(plain)
     assert np.sqrt(np.mean(filt ** 2)) < 0.05 * np.sqrt(np.mean(plain ** 2))
-    lo = wavio.synthesize(wavio.SynthSpec("sine", 8000, 16_000, frequency=200.0))
+    lo = signals.sine(8000, 16_000, 200.0)
     plain, filt = wh.decimate(lo, 4).samples, wh.decimate(lo, 4, anti_alias=True).samples
     assert np.max(np.abs(filt[100:-100] - plain[100:-100])) < 0.02
 
@@ -80,7 +81,7 @@ def test_render_reference_cases():
 # ---- test_bench.py ------------------------------------------------------------------------
 
 def small_workload():
-    sig = wavio.synthesize(wavio.SynthSpec("white_noise", 8192, 16_000.0, seed=3))
+    sig = signals.white_noise(8192, 16_000.0, seed=3)
     return sig, wh.make_scale_grid(300.0, 3000.0, 8, 16_000.0, PARAMS)
 
 

@@ -64,12 +64,20 @@ for i in range(n_cases):
         # real-Morlet rows): compare the magnitudes it encodes with the row metric instead
         got, ref = 10.0 ** (got.astype(np.float64) / 20.0), 10.0 ** (ref / 20.0)
         output = "abs"
-    if norm == "minmax" or output == "log1p":
+    if norm == "minmax":
+        # per clip 1e-5 * max/(max - min) of the un-normalised values
+        # (relative outputs) or 1e-5/(max - min) (log1p: absolute); power 2e-5, log_db in dB
+        raw = O.cwth_batch(x, scales, hop, wavelet=wavelet, output=output).reshape(clips, -1)
+        hi, lo = raw.max(axis=1), raw.min(axis=1)
+        span = np.where(hi > lo, hi - lo, np.inf)
+        base = {"log1p": 1e-5 / span, "log_db": (20.0 / np.log(10.0) * 1e-5 + 2e-5) / span,
+                "power": 2e-5 * np.abs(hi) / span}.get(output, 1e-5 * np.abs(hi) / span)
+        errs = np.abs(got.astype(np.float64) - ref).reshape(clips, -1).max(axis=1)
+        k = int(np.argmax(errs / base))
+        err, tol = float(errs[k]), float(base[k])
+    elif output == "log1p":
         err = float(np.abs(got - ref).max())
-        tol = 5e-5 if norm else 1e-5
-        if norm:  # the map amplifies by max / (max - min)
-            hi, lo = ref.max(axis=(1, 2)), ref.min(axis=(1, 2))
-            tol = tol * float(max(1.0, np.max(np.where(hi > lo, (np.abs(hi) + np.abs(lo)) / np.maximum(hi - lo, 1e-30), 1.0))))
+        tol = 1e-5
     else:
         r2 = ref.reshape(-1, ref.shape[-1])
         g2 = got.reshape(-1, got.shape[-1])
