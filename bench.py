@@ -607,6 +607,8 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG,
                     help="c1..c5 or c4h{1,16,64,256,1024} (default c5, the metric's config)")
     ap.add_argument("--engine", choices=["auto", "simt", "umma"], default="auto")
+    ap.add_argument("--norm", choices=["config", "none", "minmax"], default="config",
+                    help="override the config's normalisation (diagnostics; default: the config's)")
     ap.add_argument("--clips", type=int, default=0, help="override clips per GPU (weak) / total (strong)")
     ap.add_argument("--ref-clips", type=int, default=32, help="clips in the CPU-baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -618,6 +620,8 @@ def main():
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     w = workload(args.config)
+    if args.norm != "config":
+        w["norm"] = None if args.norm == "none" else args.norm
     world_env = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         return run_reference(args, w)

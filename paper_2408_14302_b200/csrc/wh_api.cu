@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <mutex>
+#include <thread>
+#include <vector>
 #include <string>
 
 #include "wh_internal.h"
@@ -207,6 +209,11 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_minmax); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
+    if (p->h_stage) cudaFreeHost(p->h_stage);
+    for (int i = 0; i < 2; ++i) {
+        if (p->ev_h2d[i]) cudaEventDestroy(p->ev_h2d[i]);
+        if (p->ev_d2h[i]) cudaEventDestroy(p->ev_d2h[i]);
+    }
     cudaSetDevice(cur);
     delete p;
 }
@@ -295,7 +302,7 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
             }
         }
     }
-    if (rc == WH_OK && norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA) {
+    if (rc == WH_OK && norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA && !p->minmax_2pass) {
         // write-once min-max: per-clip unit arrivals + the bitmap of units left to the fix-up
         const int64_t bits = (int64_t)((p->row_tiles + p->cg - 1) / p->cg) * (int64_t)p->passes.size() * p->cg;
         p->ab_words = (int32_t)((bits + 31) / 32);
@@ -402,7 +409,7 @@ static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x
     void *dst = render ? static_cast<void *>(scratch) : out_dev;
     // the UMMA engine normalises min-max plans inside the kernel (write-once); the SIMT
     // engine keeps the read-modify-write pass
-    const bool inkernel = p->norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA;
+    const bool inkernel = p->norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA && !p->minmax_2pass;
     if (p->norm != WH_NORM_NONE) rc = minmax_reset(*p, clips, mm, inkernel ? arrive : nullptr, abandon, s);
     if (rc == WH_OK)
         rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm, inkernel ? arrive : nullptr,
@@ -442,6 +449,127 @@ static bool is_pinned(const void *ptr) {
     return at.type == cudaMemoryTypeHost;
 }
 
+// ---- wh_execute_host pipelines ---------------------------------------------------------
+// One chunk of clips [c0, c0 + nc) on stream s: H2D of its input from `xsrc`, the plan's
+// kernels into the plan's device buffers, D2H of its output into `odst`.
+static int host_chunk(Plan *p, const float *xsrc, void *odst, int64_t c0, int64_t nc, cudaStream_t s,
+                      size_t in_clip, size_t out_clip, cudaEvent_t h2d_done = nullptr) {
+    float *dx = p->d_x + (size_t)c0 * p->N;
+    uint8_t *dout = reinterpret_cast<uint8_t *>(p->d_out) + (size_t)c0 * out_clip;
+    if (cudaMemcpyAsync(dx, xsrc, in_clip * (size_t)nc, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return fail(WH_E_CUDA, "H2D copy failed");
+    if (h2d_done && cudaEventRecord(h2d_done, s) != cudaSuccess) return fail(WH_E_CUDA, "cudaEventRecord failed");
+    int rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0, p->d_arrive ? p->d_arrive + c0 : nullptr,
+                          p->d_abandon ? p->d_abandon + (size_t)c0 * p->ab_words : nullptr,
+                          p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr,
+                          p->d_rparams ? static_cast<uint8_t *>(p->d_rparams) + (size_t)WH_RENDER_PARAM_BYTES * c0
+                                       : nullptr);
+    if (rc == WH_OK && cudaMemcpyAsync(odst, dout, out_clip * (size_t)nc, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        rc = fail(WH_E_CUDA, "D2H copy failed");
+    return rc;
+}
+
+// Pinned host buffers: clip chunks alternate over two streams so that the H2D copy of chunk
+// j+1, the kernels of chunk j and the D2H copy of chunk j-1 overlap (PCIe is full duplex).
+// The D2H copies bound the pipeline; the first chunk is small so that they start early (its
+// H2D copy and kernel are the pipeline fill), the rest are equal.
+static int host_pipeline_pinned(Plan *p, const float *x_host, int64_t clips, void *out_host, size_t in_clip,
+                                size_t out_clip) {
+    int64_t max_chunks = 8;
+    if (const char *c = diag_knob("WH_HOST_CHUNKS")) max_chunks = std::max(1, std::atoi(c));
+    const int64_t n_chunks = clips >= 4 ? std::min<int64_t>(max_chunks, clips) : 1;
+    int64_t first = clips, per = clips;
+    if (n_chunks > 1) {
+        first = std::max<int64_t>(1, clips / (4 * n_chunks));
+        if (const char *f = diag_knob("WH_HOST_FIRST")) first = std::max<int64_t>(1, std::atoi(f));
+        first = std::min(first, clips - (n_chunks - 1));
+        per = (clips - first + n_chunks - 2) / (n_chunks - 1);
+    }
+    int rc = WH_OK;
+    for (int64_t c0 = 0, j = 0, nc = first; c0 < clips && rc == WH_OK; c0 += nc, ++j, nc = per) {
+        nc = std::min(nc, clips - c0);
+        rc = host_chunk(p, x_host + (size_t)c0 * p->N, static_cast<uint8_t *>(out_host) + (size_t)c0 * out_clip, c0, nc,
+                        (j & 1) ? p->stream2 : p->stream, in_clip, out_clip);
+    }
+    return rc;
+}
+
+// memcpy split over host threads (a pageable <-> pinned copy runs at a few GB/s per core)
+static void par_copy(void *dst, const void *src, size_t bytes) {
+    const size_t kMin = (size_t)8 << 20;
+    unsigned hw = std::thread::hardware_concurrency();
+    size_t nt = std::min<size_t>(std::max(1u, std::min(hw, 8u)), (bytes + kMin - 1) / kMin);
+    if (nt <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nt && t * per < bytes; ++t)
+        th.emplace_back([=] {
+            const size_t o = t * per;
+            memcpy(static_cast<uint8_t *>(dst) + o, static_cast<const uint8_t *>(src) + o, std::min(per, bytes - o));
+        });
+    memcpy(dst, src, std::min(per, bytes));
+    for (auto &t : th) t.join();
+}
+
+// Pageable host buffers: a plan-owned pinned staging ring of two input and two output chunk
+// slots.  Per chunk j (slot j & 1): the host copies its input into the slot once the H2D copy
+// of chunk j-2 has finished, the device copies / computes / copies back into the output slot,
+// and while it does the host drains chunk j-1's output slot into the caller's buffer.
+static int host_pipeline_staged(Plan *p, const float *x_host, int64_t clips, void *out_host, size_t in_clip,
+                                size_t out_clip) {
+    const size_t target = (size_t)64 << 20;  // bytes of input + output per chunk
+    int64_t per = std::max<int64_t>(1, (int64_t)(target / (in_clip + out_clip)));
+    if (clips >= 2) per = std::min(per, (clips + 1) / 2);  // at least two chunks: overlap
+    per = std::min(per, clips);
+    const size_t slot_in = in_clip * (size_t)per, slot_out = out_clip * (size_t)per;
+    const size_t need = 2 * (slot_in + slot_out);
+    if (need > p->h_stage_bytes) {
+        if (p->h_stage) cudaFreeHost(p->h_stage);
+        p->h_stage = nullptr;
+        p->h_stage_bytes = 0;
+        if (cudaHostAlloc(reinterpret_cast<void **>(&p->h_stage), need, cudaHostAllocDefault) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return fail(WH_E_OOM, "cudaHostAlloc(staging ring) failed");
+        }
+        p->h_stage_bytes = need;
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (!p->ev_h2d[i] && cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(WH_E_CUDA, "cudaEventCreate failed");
+        if (!p->ev_d2h[i] && cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming) != cudaSuccess)
+            return fail(WH_E_CUDA, "cudaEventCreate failed");
+    }
+    uint8_t *xs[2] = {p->h_stage, p->h_stage + slot_in};
+    uint8_t *os[2] = {p->h_stage + 2 * slot_in, p->h_stage + 2 * slot_in + slot_out};
+    const int64_t n_chunks = (clips + per - 1) / per;
+    auto drain = [&](int64_t j) -> int {
+        const int k = (int)(j & 1);
+        if (cudaEventSynchronize(p->ev_d2h[k]) != cudaSuccess) return fail(WH_E_CUDA, "execute_host: D2H failed");
+        const int64_t c0 = j * per, nc = std::min(per, clips - c0);
+        par_copy(static_cast<uint8_t *>(out_host) + (size_t)c0 * out_clip, os[k], out_clip * (size_t)nc);
+        return WH_OK;
+    };
+    int rc = WH_OK;
+    for (int64_t j = 0; j < n_chunks && rc == WH_OK; ++j) {
+        const int k = (int)(j & 1);
+        const int64_t c0 = j * per, nc = std::min(per, clips - c0);
+        cudaStream_t s = k ? p->stream2 : p->stream;
+        if (j >= 2 && cudaEventSynchronize(p->ev_h2d[k]) != cudaSuccess) {
+            rc = fail(WH_E_CUDA, "execute_host: H2D failed");
+            break;
+        }
+        par_copy(xs[k], x_host + (size_t)c0 * p->N, in_clip * (size_t)nc);
+        rc = host_chunk(p, reinterpret_cast<const float *>(xs[k]), os[k], c0, nc, s, in_clip, out_clip, p->ev_h2d[k]);
+        if (rc == WH_OK && cudaEventRecord(p->ev_d2h[k], s) != cudaSuccess) rc = fail(WH_E_CUDA, "cudaEventRecord failed");
+        if (rc == WH_OK && j >= 1) rc = drain(j - 1);
+    }
+    if (rc == WH_OK) rc = drain(n_chunks - 1);
+    return rc;
+}
+
 int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out_host) {
     if (!plan) return fail(WH_E_INVALID_ARG, "plan is NULL");
     Plan *p = reinterpret_cast<Plan *>(plan);
@@ -467,43 +595,11 @@ int wh_execute_host(wh_plan *plan, const float *x_host, int64_t clips, void *out
         WH_CUDA_TRY(cudaMalloc(&p->d_out, cap));
         p->d_out_bytes = cap;
     }
-    // Pinned host buffers: pipeline clip chunks over two streams so that the H2D copy of
-    // chunk j+1, the kernel of chunk j and the D2H copy of chunk j-1 overlap (PCIe is full
-    // duplex).  Pageable buffers: one chunk (the copies are staged by the driver anyway).
     const bool pinned = is_pinned(x_host) && is_pinned(out_host);
-    int64_t max_chunks = 8;
-    if (const char *c = std::getenv("WH_HOST_CHUNKS")) max_chunks = std::max(1, std::atoi(c));  // experiments
-    const int64_t n_chunks = (pinned && clips >= 4) ? std::min<int64_t>(max_chunks, clips) : 1;
-    // The D2H copies bound the pipeline; the first chunk is small so that they start early
-    // (its H2D copy and kernel are the pipeline fill), the rest are equal.
-    int64_t first = clips, per = clips;
-    if (n_chunks > 1) {
-        first = std::max<int64_t>(1, clips / (4 * n_chunks));
-        if (const char *f = std::getenv("WH_HOST_FIRST")) first = std::max<int64_t>(1, std::atoi(f));  // experiments
-        first = std::min(first, clips - (n_chunks - 1));
-        per = (clips - first + n_chunks - 2) / (n_chunks - 1);
-    }
+    const size_t in_clip = sizeof(float) * (size_t)p->N;
     const size_t out_clip = (size_t)p->S * p->F * out_elem_bytes(*p);
-    int rc = WH_OK;
-    for (int64_t c0 = 0, j = 0, nc = first; c0 < clips && rc == WH_OK; c0 += nc, ++j, nc = per) {
-        nc = std::min(nc, clips - c0);
-        cudaStream_t s = (j & 1) ? p->stream2 : p->stream;
-        float *dx = p->d_x + (size_t)c0 * p->N;
-        uint8_t *dout = reinterpret_cast<uint8_t *>(p->d_out) + (size_t)c0 * out_clip;
-        if (cudaMemcpyAsync(dx, x_host + (size_t)c0 * p->N, sizeof(float) * (size_t)nc * p->N,
-                            cudaMemcpyHostToDevice, s) != cudaSuccess) {
-            rc = fail(WH_E_CUDA, "H2D copy failed");
-            break;
-        }
-        rc = execute_impl(p, dx, nc, p->N, dout, s, p->d_minmax + 2 * c0, p->d_arrive ? p->d_arrive + c0 : nullptr,
-                          p->d_abandon ? p->d_abandon + (size_t)c0 * p->ab_words : nullptr,
-                          p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr,
-                          p->d_rparams ? static_cast<uint8_t *>(p->d_rparams) + (size_t)WH_RENDER_PARAM_BYTES * c0
-                                       : nullptr);
-        if (rc == WH_OK && cudaMemcpyAsync(reinterpret_cast<uint8_t *>(out_host) + (size_t)c0 * out_clip, dout,
-                                           (size_t)nc * out_clip, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-            rc = fail(WH_E_CUDA, "D2H copy failed");
-    }
+    int rc = pinned ? host_pipeline_pinned(p, x_host, clips, out_host, in_clip, out_clip)
+                    : host_pipeline_staged(p, x_host, clips, out_host, in_clip, out_clip);
     const cudaError_t e1 = cudaStreamSynchronize(p->stream), e2 = cudaStreamSynchronize(p->stream2);
     if (rc == WH_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
         rc = fail(WH_E_CUDA, std::string("execute_host failed: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));

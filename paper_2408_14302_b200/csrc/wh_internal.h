@@ -128,6 +128,7 @@ struct Plan {
     double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
     bool no_convregs = false;      // UMMA planner override: converters without the register prefetch
     bool force_fixup = false;      // UMMA planner override (tests): min-max units all to the fix-up kernel
+    bool minmax_2pass = false;     // UMMA: per-clip min-max as a separate read-modify-write pass
     int32_t pgroups_force = 0;     // UMMA planner override: pass groups per tile pair (0 = modelled)
     int32_t dbg = 0;               // diagnostics role switches (WH_DIAG builds only)
     std::vector<int32_t> fexp;
@@ -157,6 +158,11 @@ struct Plan {
     void *d_out = nullptr;
     size_t d_x_bytes = 0, d_out_bytes = 0;
     cudaStream_t stream = nullptr, stream2 = nullptr;  // wh_execute_host pipeline
+    // wh_execute_host with pageable host buffers: plan-owned pinned staging ring (two input
+    // and two output chunk slots) and the events that recycle them
+    uint8_t *h_stage = nullptr;
+    size_t h_stage_bytes = 0;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
 };
 
 int64_t out_elem_bytes(const Plan &p);

@@ -1719,6 +1719,12 @@ int umma_prepare(Plan &p) {
 static int umma_prepare_impl(Plan &p) {
     p.no_convregs = plan_knob("WH_UMMA_NO_CONVREGS") != nullptr;
     p.force_fixup = plan_knob("WH_UMMA_MINMAX_FIXUP") != nullptr;
+    // per-clip min-max: the separate read-modify-write pass (k_minmax_apply, HBM-bound, c5
+    // 3.9 ms) by default -- the in-kernel write-once normalisation (units re-read from L2 once
+    // their clip is complete) measured slower on c5 (33.5 vs 28.4 ms, profiles/r02b_*): its raw
+    // tiles were mostly evicted before the re-read (ncu: 23.3 GB written, 12.1 GB read for
+    // 13.1 + 2.6 GB algorithmic) and the re-reads compete with the MMA operand traffic
+    p.minmax_2pass = plan_knob("WH_UMMA_MINMAX_INKERNEL") == nullptr;
     if (const char *e = plan_knob("WH_UMMA_PGROUPS")) p.pgroups_force = std::atoi(e);
     if (const char *d = diag_knob("WH_UMMA_DBG")) p.dbg = std::atoi(d);
     // hop | 64: rows of 64 samples, P = 64/hop frames (phases) per row; hop = 64..256 (multiple

@@ -217,7 +217,7 @@ def test_c5_sample_parity_and_minmax_range():
 
 def test_c5_full_launch_4096_clips():
     """The launch the bench times: all 4096 c5 clips in one wh_execute.  Every clip's
-    normalised scalogram spans exactly [0, 1] (write-once in-kernel min-max), and clips 0,
+    normalised scalogram spans exactly [0, 1] (per-clip min-max), and clips 0,
     2048 and 4095 match the oracle (32-bit unit math, clip counters and min-max slices at full
     size)."""
     cfg = synth.CONFIGS[5]
@@ -245,10 +245,11 @@ def test_c5_full_launch_4096_clips():
 
 @pytest.mark.parametrize("output", ["abs", "log1p"])
 def test_write_once_minmax_fixup_path_is_byte_identical(output, monkeypatch):
-    """Units the kernel could not normalise itself (their clip still running elsewhere
+    """The write-once variant (WH_UMMA_MINMAX_INKERNEL=1): units the kernel could not normalise itself (their clip still running elsewhere
     after a bounded wait) go to the fix-up kernel; forcing every unit down that path
     (WH_UMMA_MINMAX_FIXUP=1, a planner override) gives byte-identical output, and both match
     the SIMT engine's read-modify-write pass within tolerance."""
+    monkeypatch.setenv("WH_UMMA_MINMAX_INKERNEL", "1")  # the write-once variant (planner option)
     x = synth.make_batch(5, clips=5, n=50000, start=7)
     sc = synth.config_scales(5)
     mk = lambda: wh.CwthPlan(sc, None, 32, 50000, wavelet="cmor", output=output, norm="minmax",  # noqa: E731
@@ -262,6 +263,12 @@ def test_write_once_minmax_fixup_path_is_byte_identical(output, monkeypatch):
     assert plan.launches(5) == 3
     plan.close()
     assert inkernel.tobytes() == fixup.tobytes()
+    monkeypatch.delenv("WH_UMMA_MINMAX_INKERNEL")
+    monkeypatch.delenv("WH_UMMA_MINMAX_FIXUP")
+    plan = mk()
+    twopass = plan.execute_host(x).copy()  # the default: a separate read-modify-write pass
+    plan.close()
+    assert twopass.tobytes() == inkernel.tobytes()
     ref = O.cwth_batch(x, sc, 32, wavelet="cmor", output=output, norm="minmax")
     raw = O.cwth_batch(x, sc, 32, wavelet="cmor", output=output)
     check_minmax(inkernel, ref, raw, output)
@@ -340,6 +347,25 @@ def test_device_and_host_paths_identical():
     dev = plan.execute(torch.from_numpy(x).cuda()).cpu().numpy()
     np.testing.assert_array_equal(host, dev)
     assert plan.launches(3) == 1
+
+
+@pytest.mark.parametrize("norm", [None, "minmax"])
+def test_pageable_staged_and_pinned_host_paths_identical(norm):
+    """wh_execute_host with pageable numpy buffers runs through the plan's pinned staging
+    ring in clip chunks of ~64 MB (c2 shape: 33 clips per chunk, 100 clips = 4 chunks, the two
+    slots recycled by events); the result is byte-identical to the pinned pipeline and to the
+    device path."""
+    n = 160000
+    x = synth.make_batch(2, clips=100, n=n, start=3)
+    sc = synth.config_scales(2)
+    plan = wh.CwthPlan(sc, None, 64, n, wavelet="rmor", output="log1p", norm=norm, max_clips=100)
+    pageable = plan.execute_host(x).copy()
+    xpin = torch.from_numpy(x).pin_memory()
+    opin = torch.empty(pageable.shape, dtype=torch.float32).pin_memory()
+    plan.execute_host(xpin.numpy(), opin.numpy())
+    dev = plan.execute(torch.from_numpy(x).cuda()).cpu().numpy()
+    plan.close()
+    assert pageable.tobytes() == opin.numpy().tobytes() == dev.tobytes()
 
 
 # ---------------------------------------------------------------------------------------

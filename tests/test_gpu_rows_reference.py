@@ -128,6 +128,12 @@ def test_bench_json_and_extrapolation():
 
 # ---- test_cli.py ---------------------------------------------------------------------------
 
+def wav_of(tmp_path, name, sig):
+    path = tmp_path / name
+    wavio.write_wav(sig, path, encoding="float32")
+    return str(path)
+
+
 def test_transform_commands(tmp_path, capsys):
     wav = tmp_path / "in.wav"
     make_wav(wav, n=160_000)
@@ -136,21 +142,24 @@ def test_transform_commands(tmp_path, capsys):
                     "--scales", "8", "--fmin", "500", "--fmax", "4000"]) == 0
     m = S.read_matrix_bin(out)
     assert (m.columns, m.hop, m.rows) == (1250, 128, 8)
-    assert run_cli(["transform", "sine:frequency=1000", "--length", "4096", "--rate", "16000",
-                    "--out", str(out), "--hop", "64", "--scales", "6", "--fmin", "500", "--fmax", "4000"]) == 0
+    sine = wav_of(tmp_path, "sine.wav", signals.sine(4096, 16_000, 1000.0, 0.5))
+    assert run_cli(["transform", sine, "--out", str(out), "--hop", "64", "--scales", "6", "--fmin", "500",
+                    "--fmax", "4000"]) == 0
     assert S.read_matrix_bin(out).columns == 64
-    assert run_cli(["transform", "noise:seed=1", "--length", "16000", "--rate", "16000", "--out", str(out),
-                    "--mode", "decimate", "--hop", "4", "--scales", "6", "--fmin", "100", "--fmax", "1500"]) == 0
+    n1 = wav_of(tmp_path, "n1.wav", signals.white_noise(16000, 16_000, 1))
+    assert run_cli(["transform", n1, "--out", str(out), "--mode", "decimate", "--hop", "4", "--scales", "6",
+                    "--fmin", "100", "--fmax", "1500"]) == 0
     m = S.read_matrix_bin(out)
     assert (m.source_rate, m.hop, m.columns) == (4000.0, 4, 4000)
-    assert run_cli(["transform", "noise:seed=2", "--length", "2048", "--rate", "16000", "--out", str(out),
-                    "--mode", "full", "--scales", "4", "--fmin", "500", "--fmax", "4000"]) == 0
+    n2 = wav_of(tmp_path, "n2.wav", signals.white_noise(2048, 16_000, 2))
+    assert run_cli(["transform", n2, "--out", str(out), "--mode", "full", "--scales", "4", "--fmin", "500",
+                    "--fmax", "4000"]) == 0
     m = S.read_matrix_bin(out)
     assert (m.columns, m.hop) == (2048, 1)
     csv, pgm = tmp_path / "o.csv", tmp_path / "o.pgm"
-    assert run_cli(["transform", "noise:seed=4", "--length", "2000", "--rate", "16000", "--out", str(out),
-                    "--csv", str(csv), "--pgm", str(pgm), "--hop", "50", "--scales", "5", "--fmin", "500",
-                    "--fmax", "4000", "--mag", "log_db"]) == 0
+    n4 = wav_of(tmp_path, "n4.wav", signals.white_noise(2000, 16_000, 4))
+    assert run_cli(["transform", n4, "--out", str(out), "--csv", str(csv), "--pgm", str(pgm), "--hop", "50",
+                    "--scales", "5", "--fmin", "500", "--fmax", "4000", "--mag", "log_db"]) == 0
     assert csv.read_text().count("\n") == 5
     assert pgm.read_bytes().startswith(b"P5\n40 5\n255\n")
     assert run_cli(["transform", str(tmp_path / "none.wav"), "--out", str(tmp_path / "x.scg1")]) == 1
@@ -158,8 +167,9 @@ def test_transform_commands(tmp_path, capsys):
 
 
 def test_transform_byte_deterministic(tmp_path):
-    args = ["transform", "noise:seed=5", "--length", "3000", "--rate", "16000", "--mode", "strided",
-            "--hop", "30", "--scales", "6", "--fmin", "300", "--fmax", "3000"]
+    n5 = wav_of(tmp_path, "n5.wav", signals.white_noise(3000, 16_000, 5))
+    args = ["transform", n5, "--mode", "strided", "--hop", "30", "--scales", "6", "--fmin", "300",
+            "--fmax", "3000"]
     outs = []
     for tag in ("a", "b"):
         o, p = tmp_path / f"{tag}.scg1", tmp_path / f"{tag}.pgm"
@@ -170,8 +180,11 @@ def test_transform_byte_deterministic(tmp_path):
 
 def test_scalogram_command_and_flip(tmp_path):
     out = tmp_path / "o.scg1"
-    run_cli(["transform", "chirp:f0=200,f1=4000", "--length", "4000", "--rate", "16000", "--out", str(out),
-             "--hop", "40", "--scales", "6", "--fmin", "300", "--fmax", "3000"])
+    t = np.arange(4000) / 16_000.0
+    chirp = wh.SignalBuffer(np.sin(2 * np.pi * (200.0 * t + 0.5 * (3800.0 / t[-1]) * t * t)), 16_000.0)
+    src = wav_of(tmp_path, "chirp.wav", chirp)
+    run_cli(["transform", src, "--out", str(out), "--hop", "40", "--scales", "6", "--fmin", "300",
+             "--fmax", "3000"])
     a, b = tmp_path / "a.pgm", tmp_path / "b.pgm"
     assert run_cli(["scalogram", str(out), "--out", str(a)]) == 0
     assert a.read_bytes().startswith(b"P5\n100 6\n255\n")
@@ -180,7 +193,7 @@ def test_scalogram_command_and_flip(tmp_path):
 
 
 def test_usage_errors(capsys):
-    assert run_cli(["transform", "noise", "--out", "x.scg1", "--bogus"]) == 2
+    assert run_cli(["transform", "x.wav", "--out", "x.scg1", "--bogus"]) == 2
     assert "usage" in capsys.readouterr().err.lower()
     assert run_cli([]) == 2
     assert run_cli(["fourier"]) == 2
