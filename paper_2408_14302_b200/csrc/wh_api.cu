@@ -120,6 +120,24 @@ __global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip,
         base[i] = constant ? 0.0f : (base[i] - lo) * sc;
 }
 
+// ---------------------------------------------------------------------------------------
+// Non-finite input samples (SIMT engine): the exact values of the coefficients they reach
+// (nf_fixup_clip); a block per clip, exiting at once for clips without any.
+__global__ void k_nf_fixup(NfArgs a, int64_t clips) {
+    for (int64_t b = blockIdx.x; b < clips; b += gridDim.x) nf_fixup_clip(a, b, threadIdx.x, blockDim.x);
+}
+
+int nf_fixup_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, uint32_t *mm, uint32_t *bad,
+                    cudaStream_t s) {
+    NfArgs a{};
+    a.x = x; a.ld_x = ld_x; a.N = p.N; a.hop = p.hop; a.F = p.F; a.S = p.S;
+    a.wavelet = p.wavelet; a.output = p.output; a.scales = p.d_scales; a.half = p.d_half;
+    a.C = p.C; a.Bw = p.B; a.out = out; a.mm = mm; a.bad = bad;
+    k_nf_fixup<<<(unsigned)std::min<int64_t>(clips, 4 * (int64_t)p.sms), 128, 0, s>>>(a, clips);
+    WH_CUDA_TRY(cudaGetLastError());
+    return WH_OK;
+}
+
 int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, uint32_t *arrive, uint32_t *abandon, cudaStream_t s) {
     k_minmax_reset<<<(unsigned)((clips + 255) / 256), 256, 0, s>>>(mm, arrive, abandon, p.ab_words, clips);
     WH_CUDA_TRY(cudaGetLastError());
@@ -206,7 +224,7 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
     cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
     cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow); cudaFree(p->d_tables);
-    cudaFree(p->d_minmax); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
+    cudaFree(p->d_minmax); cudaFree(p->d_nfbad); cudaFree(p->d_nfctl); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     if (p->h_stage) cudaFreeHost(p->h_stage);
@@ -275,6 +293,12 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
     p->max_clips = max_clips; p->output = output; p->norm = norm;
 
     int rc = build_fold_bank(*p);
+    if (rc == WH_OK) {  // non-finite sample records, zeroed once (each fix-up resets what it used)
+        const size_t nb = sizeof(uint32_t) * (size_t)max_clips * (1 + WH_NF_CAP), nc = sizeof(uint32_t) * 2 * (size_t)max_clips;
+        if (cudaMalloc(&p->d_nfbad, nb) != cudaSuccess || cudaMalloc(&p->d_nfctl, nc) != cudaSuccess ||
+            cudaMemset(p->d_nfbad, 0, nb) != cudaSuccess || cudaMemset(p->d_nfctl, 0, nc) != cudaSuccess)
+            rc = fail(WH_E_OOM, "cudaMalloc(non-finite records) failed");
+    }
     if (rc == WH_OK && norm != WH_NORM_NONE) {
         if (cudaMalloc(&p->d_minmax, sizeof(uint32_t) * 2 * max_clips) != cudaSuccess)
             rc = fail(WH_E_OOM, "cudaMalloc(minmax) failed");
@@ -356,7 +380,9 @@ int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches) {
     // engine + (min/max reset + normalise) or (reset + map parameters + uint8 map)
     // min-max: reset + (UMMA: the fix-up check | SIMT: the normalise pass)
     const int mm = p->norm == WH_NORM_MINMAX ? 2 : 0;
-    *launches = clips > 0 ? (1 + mm + (is_render(*p) ? 3 : 0)) : 0;
+    // + the SIMT engine's non-finite fix-up (the UMMA engine's last CTA does it in-kernel)
+    const int nf = p->engine == WH_ENGINE_UMMA ? 0 : 1;
+    *launches = clips > 0 ? (1 + nf + mm + (is_render(*p) ? 3 : 0)) : 0;
     return WH_OK;
 }
 
@@ -403,8 +429,11 @@ int wh_plan_taps(const wh_plan *plan, int32_t scale_index, float *re, float *im,
 // values a render plan maps to uint8
 // arrive: this call's slice of the per-clip unit arrival counters (UMMA write-once min-max)
 static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x, void *out_dev, cudaStream_t s,
-                        uint32_t *mm, uint32_t *arrive, uint32_t *abandon, float *scratch, void *rparams) {
+                        uint32_t *mm, uint32_t *arrive, uint32_t *abandon, float *scratch, void *rparams, int64_t c0) {
     int rc = WH_OK;
+    // this launch's slices of the non-finite-sample records (c0: its first clip in the plan's
+    // per-clip arrays)
+    uint32_t *nfbad = p->d_nfbad + c0 * (int64_t)(1 + WH_NF_CAP), *nfctl = p->d_nfctl + 2 * c0;
     const bool render = is_render(*p);
     void *dst = render ? static_cast<void *>(scratch) : out_dev;
     // the UMMA engine normalises min-max plans inside the kernel (write-once); the SIMT
@@ -413,8 +442,12 @@ static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x
     if (p->norm != WH_NORM_NONE) rc = minmax_reset(*p, clips, mm, inkernel ? arrive : nullptr, abandon, s);
     if (rc == WH_OK)
         rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm, inkernel ? arrive : nullptr,
-                                                         abandon)
-                                           : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm);
+                                                         abandon, nfbad, nfctl)
+                                           : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm, nfbad, nfctl);
+    // the SIMT engine's non-finite fix-up is a kernel of its own (the UMMA engine's last CTA
+    // does it)
+    if (rc == WH_OK && p->engine != WH_ENGINE_UMMA)
+        rc = nf_fixup_launch(*p, x_dev, clips, ld_x, dst, p->norm != WH_NORM_NONE ? mm : nullptr, nfbad, s);
     if (rc == WH_OK && p->norm == WH_NORM_MINMAX && !inkernel) rc = minmax_apply(*p, clips, out_dev, mm, s);
     if (rc == WH_OK && render)
         rc = render_apply(scratch, clips, p->S, p->F, mm, rparams, p->norm == WH_NORM_RENDER_U8 ? 1 : 0,
@@ -435,7 +468,7 @@ int wh_execute(wh_plan *plan, const float *x_dev, int64_t clips, int64_t ld_x, v
     cudaGetDevice(&prev);
     if (prev != p->device) WH_CUDA_TRY(cudaSetDevice(p->device));
     const int rc = execute_impl(p, x_dev, clips, ld_x, out_dev, s, p->d_minmax, p->d_arrive, p->d_abandon,
-                                p->d_scratch, p->d_rparams);
+                                p->d_scratch, p->d_rparams, 0);
     if (prev != p->device) cudaSetDevice(prev);
     return rc;
 }
@@ -463,7 +496,8 @@ static int host_chunk(Plan *p, const float *xsrc, void *odst, int64_t c0, int64_
                           p->d_abandon ? p->d_abandon + (size_t)c0 * p->ab_words : nullptr,
                           p->d_scratch ? p->d_scratch + (size_t)c0 * p->S * p->F : nullptr,
                           p->d_rparams ? static_cast<uint8_t *>(p->d_rparams) + (size_t)WH_RENDER_PARAM_BYTES * c0
-                                       : nullptr);
+                                       : nullptr,
+                          c0);
     if (rc == WH_OK && cudaMemcpyAsync(odst, dout, out_clip * (size_t)nc, cudaMemcpyDeviceToHost, s) != cudaSuccess)
         rc = fail(WH_E_CUDA, "D2H copy failed");
     return rc;

@@ -30,6 +30,9 @@ inline const char *diag_knob(const char *name) {
 #endif
 }
 
+// non-finite samples tracked per clip (beyond: every coefficient of the clip is NaN)
+constexpr int WH_NF_CAP = 1024;
+
 // Thread-local last-error message behind wh_last_error().
 void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
@@ -150,6 +153,11 @@ struct Plan {
     uint32_t *d_arrive = nullptr;  // UMMA write-once min-max: [max_clips] unit arrivals per clip
     uint32_t *d_abandon = nullptr; // UMMA write-once min-max: [max_clips][ab_words] units left to the fix-up
     int32_t ab_words = 0;
+    // non-finite input samples (NaN / +-inf): the engines compute with them replaced by 0 and
+    // record their positions; a fix-up then writes the exact IEEE value of every coefficient
+    // whose support contains one (the reference's propagation, wavelet.py:264-270)
+    uint32_t *d_nfbad = nullptr;   // [max_clips][1 + WH_NF_CAP]: count, positions
+    uint32_t *d_nfctl = nullptr;   // [max_clips][2]: per-launch CTA counter (slot of the launch's first clip), any-flag
     float *d_scratch = nullptr;    // render plans: float values [max_clips][S][F] before the uint8 map
     void *d_rparams = nullptr;     // render plans: WH_RENDER_PARAM_BYTES per clip
 
@@ -172,11 +180,12 @@ int build_fold_bank(Plan &p);
 
 // engines
 int simt_prepare(Plan &p);
-int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm);
+int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
+                uint32_t *nfbad, uint32_t *nfctl);
 int umma_supported(const Plan &p, std::string *why);
 int umma_prepare(Plan &p);
 int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
-                uint32_t *arrive, uint32_t *abandon);
+                uint32_t *arrive, uint32_t *abandon, uint32_t *nfbad, uint32_t *nfctl);
 
 // epilogue helpers (wh_api.cu)
 int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, uint32_t *arrive, uint32_t *abandon, cudaStream_t s);
@@ -185,6 +194,8 @@ int render_apply(const float *values, int64_t clips, int64_t rows, int64_t cols,
                  int32_t flip, uint8_t *out, cudaStream_t s);
 inline bool is_render(const Plan &p) { return p.norm == WH_NORM_RENDER_U8 || p.norm == WH_NORM_RENDER_U8_NOFLIP; }
 int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s);
+int nf_fixup_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, uint32_t *mm, uint32_t *bad,
+                    cudaStream_t s);
 
 }  // namespace wh
 
@@ -211,6 +222,127 @@ __device__ __forceinline__ float apply_output(float mag, int output) {
 }
 __device__ __forceinline__ float magnitude(float re, float im, int wavelet) {
     return wavelet == WH_WAVELET_RMOR ? fabsf(re) : sqrtf(fmaf(re, re, im * im));
+}
+__device__ __forceinline__ bool is_finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
+// max that propagates NaN (and +inf through |x|): one test per window finds non-finite input
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+// Record non-finite sample `pos` of a clip (bad = the clip's [1 + WH_NF_CAP] record) and
+// flag the launch (any = its control word).
+__device__ __forceinline__ void nf_record(uint32_t *bad, uint32_t *any, int64_t pos) {
+    const uint32_t i = atomicAdd(bad, 1u);
+    if (i < (uint32_t)WH_NF_CAP) bad[1 + i] = (uint32_t)pos;
+    atomicOr(any, 1u);
+}
+
+struct NfArgs {
+    const float *x;             // the launch's input [clips][ld_x]
+    int64_t ld_x, N, hop, F;
+    int32_t S, wavelet, output;
+    const double *scales;
+    const int64_t *half;
+    double C, Bw;
+    void *out;                  // [clips][S][F] float or float2 (complex64)
+    uint32_t *mm;               // per-clip min/max keys or nullptr
+    uint32_t *bad;              // [clips][1 + WH_NF_CAP]
+};
+
+// Exact value of every coefficient of clip b whose support [kH - L_s, kH + L_s] holds a
+// recorded non-finite sample, as the reference's default (numba) backend gives it: the
+// finite samples cannot change a sum that contains +-inf or NaN, so each part is the sum over
+// the non-finite samples in the support of x_t * tap(t - kH) in IEEE double (inf * 0 = NaN,
+// inf - inf = NaN), then the output map.  The engines' values of
+// these coefficients (computed with the samples replaced by 0) are overwritten; the clip's
+// min / max keys take the new values (NaN orders above +inf: a NaN clip normalises to NaN,
+// an inf clip to 0 / NaN as (v - lo) / (hi - lo) does in float).  More than WH_NF_CAP
+// non-finite samples: the whole clip is NaN.  Block-wide; resets the clip's record.
+__device__ inline void nf_fixup_clip(const NfArgs &a, int64_t b, int tid, int nthreads) {
+    uint32_t *rec = a.bad + b * (int64_t)(1 + WH_NF_CAP);
+    const uint32_t cnt = rec[0];
+    if (cnt == 0) return;
+    const float *xb = a.x + b * a.ld_x;
+    float *o32 = reinterpret_cast<float *>(a.out) + b * (int64_t)a.S * a.F;
+    float2 *o64 = reinterpret_cast<float2 *>(a.out) + b * (int64_t)a.S * a.F;
+    const float qnan = __uint_as_float(0x7fc00000u);
+    auto put = [&](int64_t idx, float re, float im, float v) {
+        if (a.output == WH_OUT_COMPLEX64) {
+            o64[idx] = make_float2(re, im);
+        } else {
+            o32[idx] = v;
+            if (a.mm) {
+                atomicMin(a.mm + 2 * b, f2key(v));
+                atomicMax(a.mm + 2 * b + 1, f2key(v));
+            }
+        }
+    };
+    if (cnt > (uint32_t)WH_NF_CAP) {
+        for (int64_t i = tid; i < (int64_t)a.S * a.F; i += nthreads) put(i, qnan, qnan, qnan);
+    } else {
+        const double norm = rsqrt(M_PI * a.Bw);
+        const double w = 2.0 * M_PI * a.C;
+        for (uint32_t i = 0; i < cnt; ++i) {
+            const int64_t t = rec[1 + i];
+            for (int s = tid; s < a.S; s += nthreads) {
+                const int64_t L = a.half[s];
+                const double sa = a.scales[s], rs = sqrt(sa);
+                int64_t k0 = t - L <= 0 ? 0 : (t - L + a.hop - 1) / a.hop;
+                int64_t k1 = (t + L) / a.hop;
+                if (k1 > a.F - 1) k1 = a.F - 1;
+                for (int64_t k = k0; k <= k1; ++k) {
+                    const int64_t c = k * a.hop;
+                    // owned by the first recorded sample in this coefficient's support
+                    bool first = true;
+                    for (uint32_t j = 0; j < i && first; ++j) {
+                        const int64_t tj = rec[1 + j];
+                        first = !(tj >= c - L && tj <= c + L);
+                    }
+                    if (!first) continue;
+                    // the reference's folded kernel (_kernels.py:93-112) has no imaginary tap at
+                    // u = 0 (a sample never meets im_0 there), and it assembles re + 1j * im
+                    // (wavelet.py:270), whose 0 * im turns the real part into NaN wherever the
+                    // imaginary part is not finite
+                    double re = 0.0, im = 0.0;
+                    bool imbad = false;
+                    for (uint32_t j = i; j < cnt; ++j) {
+                        const int64_t tj = rec[1 + j];
+                        const int64_t u = tj - c;
+                        if (u < -L || u > L) continue;
+                        const double xv = (double)xb[tj];
+                        const double tt = (double)(u < 0 ? -u : u) / sa;
+                        const double env = norm * exp(-(tt * tt) / a.Bw);
+                        re += xv * (env * cos(w * tt) / rs);
+                        if (u != 0) {
+                            const double ti = env * sin(w * tt) / rs;
+                            im += xv * (u < 0 ? -ti : ti);
+                            imbad = true;
+                        }
+                    }
+                    const float ore = (imbad && !isfinite(im)) ? qnan : (isnan(re) ? qnan : (float)re);
+                    const int64_t idx = (int64_t)s * a.F + k;
+                    if (a.output == WH_OUT_COMPLEX64) {
+                        if (a.wavelet == WH_WAVELET_RMOR) o64[idx] = make_float2(ore, 0.0f);
+                        else if (imbad) o64[idx] = make_float2(ore, isnan(im) ? qnan : (float)im);
+                        else o64[idx].x = ore;  // the imaginary part stays the engine's (finite) value
+                        continue;
+                    }
+                    float mag;
+                    if (a.wavelet == WH_WAVELET_RMOR) {
+                        mag = fabsf(ore);
+                    } else {
+                        const bool iminf = imbad && isinf(im);
+                        mag = (isinf(ore) || iminf) ? INFINITY : qnan;  // hypot(+-inf, any) = inf
+                    }
+                    const float v = apply_output(mag, a.output);
+                    put(idx, 0.0f, 0.0f, isnan(v) ? qnan : v);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) rec[0] = 0;
 }
 }  // namespace wh
 #endif

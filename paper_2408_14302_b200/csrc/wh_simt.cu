@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(SIMT_THREADS)
 k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_t F,
        const SimtGroup *__restrict__ groups, const SimtItem *__restrict__ items,
        const float *__restrict__ gtaps, int32_t S, int32_t wavelet, int32_t output,
-       void *__restrict__ out, uint32_t *__restrict__ minmax, int32_t tf_all) {
+       void *__restrict__ out, uint32_t *__restrict__ minmax, int32_t tf_all, uint32_t *__restrict__ nfbad,
+       uint32_t *__restrict__ nfany) {
     extern __shared__ float xs[];
     const int64_t b = blockIdx.x;
     const SimtItem it = items[blockIdx.y];
@@ -74,9 +75,17 @@ k_simt(const float *__restrict__ x, int64_t ld_x, int64_t N, int64_t hop, int64_
     const int64_t seg_start = k0 * hop - LM;
     const int64_t seg_len = (int64_t)(nf - 1) * hop + 2 * LM + 1;
     const float *xb = x + b * ld_x;
+    // non-finite samples are staged as 0 and recorded once (by the first chunk's item whose
+    // frames own the sample) for the fix-up kernel
+    const int64_t own_lo = k0 == 0 ? 0 : k0 * hop, own_hi = k0 + nf >= F ? N : (k0 + nf) * hop;
     for (int64_t i = threadIdx.x; i < seg_len; i += SIMT_THREADS) {
         int64_t g = seg_start + i;
-        xs[i] = (g >= 0 && g < N) ? __ldg(xb + g) : 0.0f;
+        float v = (g >= 0 && g < N) ? __ldg(xb + g) : 0.0f;
+        if (!is_finite_f(v)) {
+            if (it.g0 == 0 && g >= own_lo && g < own_hi) nf_record(nfbad + b * (int64_t)(1 + WH_NF_CAP), nfany, g);
+            v = 0.0f;
+        }
+        xs[i] = v;
     }
     __syncthreads();
 
@@ -241,12 +250,18 @@ int simt_prepare(Plan &p) {
     WH_CUDA_TRY(cudaGetLastError());
     const size_t smem = sizeof(float) * ((size_t)(tf - 1) * p.hop + 2 * Lmax_all + 1);
     p.smem_bytes = smem;
-    WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the attribute belongs to the kernel, which every SIMT plan shares: raise it to the device
+    // limit (a later plan with a smaller segment would otherwise lower it under this one)
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device);
+    if ((int64_t)smem > optin) return fail(WH_E_UNSUPPORTED, "SIMT segment exceeds shared memory");
+    WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    WH_CUDA_TRY(cudaFuncSetAttribute(k_simt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     return WH_OK;
 }
 
-int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm) {
+int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
+                uint32_t *nfbad, uint32_t *nfctl) {
     if (clips > 2147483647LL) return fail(WH_E_INVALID_ARG, "too many clips");
     dim3 grid((unsigned)clips, (unsigned)p.n_items);
     bool cplx = p.wavelet == WH_WAVELET_CMOR;
@@ -254,10 +269,10 @@ int simt_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     if (cplx)
         k_simt<true><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
-                                                             p.d_group_taps, p.S, p.wavelet, p.output, out, mm, p.simt_tf);
+                                                             p.d_group_taps, p.S, p.wavelet, p.output, out, mm, p.simt_tf, nfbad, nfctl + 1);
     else
         k_simt<false><<<grid, SIMT_THREADS, p.smem_bytes, s>>>(x, ld_x, p.N, p.hop, p.F, p.d_groups, p.d_items,
-                                                              p.d_group_taps, p.S, p.wavelet, p.output, out, mm, p.simt_tf);
+                                                              p.d_group_taps, p.S, p.wavelet, p.output, out, mm, p.simt_tf, nfbad, nfctl + 1);
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }

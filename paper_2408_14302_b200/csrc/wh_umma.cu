@@ -92,6 +92,11 @@ struct UmmaArgs {
     uint32_t *abandon;              // per clip ab_words words: units left to k_minmax_fixup
     int32_t ab_words;               // bit ((tile pair * pgroups + pass group) * CG + CTA rank)
     int32_t force_fixup;            // planner override (tests): every unit goes to the fix-up
+    uint32_t *nfbad;                // non-finite samples: per clip [1 + WH_NF_CAP] records
+    uint32_t *nfctl;                // [0] CTAs done (the last one runs the fix-up), [1] any recorded
+    const double *scales;           // for the fix-up's exact taps
+    const int64_t *half;
+    double Cw, Bw;
     uint32_t ring_bytes, win_half_bytes;
     int32_t out_vec_ok;             // output base 16B aligned and F % 4 == 0
     int32_t out_vec8_ok;            // output base 32B aligned and F % 8 == 0 (256-bit stores)
@@ -745,6 +750,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     constexpr int CONV_RC = 10;
     float cv[CONV_RC][8];
     float cmx = 0.0f;
+    bool cbad = false;  // this thread's chunks of the fetched window held non-finite samples
     auto conv_load8 = [&](const float *xb, int64_t w0, int32_t off, int32_t in_lo, int32_t in_hi, float (&o)[8]) {
         if (A.vec_ok && off >= in_lo && off + 8 <= in_hi) {
             const float4 *g = reinterpret_cast<const float4 *>(xb + w0 + off);
@@ -789,12 +795,46 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             float t[8];
             conv_load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(t[k]));
+            for (int k = 0; k < 8; ++k) mx = fmax_nan(mx, fabsf(t[k]));
         }
 #pragma unroll
         for (int i = 0; i < CONV_RC; ++i)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(cv[i][k]));
+            for (int k = 0; k < 8; ++k) mx = fmax_nan(mx, fabsf(cv[i][k]));
+        cbad = !(mx <= 3.402823466e38f);
+        if (cbad) {
+            // non-finite samples (rare): replaced by 0 here and after the wait; recorded for the
+            // fix-up once -- by the tile that owns the sample, in the unit of pass group 0
+            int p0, p1;
+            unit_passes(item, p0, p1);
+            const int64_t own0 = tile * 128 * A.V, own1 = own0 + 128 * (int64_t)A.V;
+            uint32_t *rec = A.nfbad + b * (int64_t)(1 + WH_NF_CAP);
+            auto fix8 = [&](int c, float (&o)[8]) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (!is_finite_f(o[k])) {
+                        const int64_t g = w0 + chunk_off(c) + k;
+                        if (p0 == 0 && g >= own0 && g < own1 && A.nfbad) nf_record(rec, A.nfctl + 1, g);
+                        o[k] = 0.0f;
+                    }
+                }
+            };
+            mx = 0.0f;
+            for (int c = ct + CONV_RC * UM_CONV_THREADS; c < chunks; c += UM_CONV_THREADS) {
+                float t[8];
+                conv_load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
+                fix8(c, t);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(t[k]));
+            }
+#pragma unroll
+            for (int i = 0; i < CONV_RC; ++i) {
+                const int c = ct + i * UM_CONV_THREADS;
+                if (c < chunks) fix8(c, cv[i]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(cv[i][k]));
+            }
+        }
         cmx = mx;
     };
     // L2 prefetch of a unit's fp32 window (one bulk prefetch: the window is a contiguous sample
@@ -1184,6 +1224,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     float t[8];
                     uint32_t hw[4], lw[4];
                     load8(xb, w0, chunk_off(c), in_lo, in_hi, t);
+                    if (cbad)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) t[k] = is_finite_f(t[k]) ? t[k] : 0.0f;
                     split8(t, sc, hw, lw);
                     put(c, hw, lw);
                 }
@@ -1240,15 +1283,30 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 chunk_rc(A, c, row, cc);
                 return row * A.V + cc * 8;
             };
-            // pass 1: max |x| over the window
+            // pass 1: max |x| over the window (NaN-propagating: one test finds non-finite input)
             float mx = 0.0f;
 #pragma unroll 4
             for (int c = ct; c < chunks; c += UM_CONV_THREADS) {
                 float v[8];
                 load8(chunk_off(c), v);
-                mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3]))),
-                                     fmaxf(fmaxf(fabsf(v[4]), fabsf(v[5])), fmaxf(fabsf(v[6]), fabsf(v[7])))));
+                mx = fmax_nan(mx, fmax_nan(fmax_nan(fmax_nan(fabsf(v[0]), fabsf(v[1])), fmax_nan(fabsf(v[2]), fabsf(v[3]))),
+                                           fmax_nan(fmax_nan(fabsf(v[4]), fabsf(v[5])), fmax_nan(fabsf(v[6]), fabsf(v[7])))));
             }
+            // non-finite samples (rare): excluded from the max here, replaced by 0 and recorded
+            // in pass 2
+            const bool tbad = !(mx <= 3.402823466e38f);
+            if (tbad) {
+                mx = 0.0f;
+                for (int c = ct; c < chunks; c += UM_CONV_THREADS) {
+                    float v[8];
+                    load8(chunk_off(c), v);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, is_finite_f(v[k]) ? fabsf(v[k]) : 0.0f);
+                }
+            }
+            int p0s, p1s;
+            unit_passes(item, p0s, p1s);
+            const int64_t own0 = tile * 128 * A.V, own1 = own0 + 128 * (int64_t)A.V;
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
             if (lane == 0) red[cw] = mx;
@@ -1271,6 +1329,17 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const int panel = cc >> 3, c8 = cc & 7;
                 float v[8];
                 load8(row * A.V + cc * 8, v);
+                if (tbad) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (!is_finite_f(v[k])) {
+                            const int64_t g = w0 + row * A.V + cc * 8 + k;
+                            if (p0s == 0 && g >= own0 && g < own1 && A.nfbad)
+                                nf_record(A.nfbad + b * (int64_t)(1 + WH_NF_CAP), A.nfctl + 1, g);
+                            v[k] = 0.0f;
+                        }
+                    }
+                }
                 uint32_t hw[4], lw[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -1500,6 +1569,31 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
         else
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+    // Non-finite input samples: the last CTA to finish writes the exact values of the
+    // coefficients they reach (nf_fixup_clip) -- normally it finds the launch's flag clear
+    if (A.nfctl) {
+        __shared__ int s_nf_last;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_nf_last = atomicAdd(A.nfctl, 1u) == gridDim.x - 1 ? 1 : 0;
+        }
+        __syncthreads();
+        if (s_nf_last) {
+            __threadfence();
+            if (*reinterpret_cast<volatile uint32_t *>(A.nfctl + 1)) {
+                NfArgs na{};
+                na.x = A.x; na.ld_x = A.ld_x; na.N = A.N; na.hop = A.hop; na.F = A.F; na.S = A.S;
+                na.wavelet = A.wavelet; na.output = A.output; na.scales = A.scales; na.half = A.half;
+                na.C = A.Cw; na.Bw = A.Bw; na.out = A.out; na.mm = A.minmax; na.bad = A.nfbad;
+                for (int64_t b = 0; b < A.clips; ++b) nf_fixup_clip(na, b, threadIdx.x, blockDim.x);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                A.nfctl[0] = 0u;
+                A.nfctl[1] = 0u;
+            }
+        }
     }
 }
 
@@ -2124,7 +2218,11 @@ static int umma_prepare_impl(Plan &p) {
     WH_CUDA_TRY(cudaGetLastError());
     WH_CUDA_TRY(cudaDeviceSynchronize());
     cudaFree(d_fexp);
-    WH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes));
+    // the attribute belongs to the kernel instantiation, which other plans share: raise it to the
+    // device limit once instead of to this plan's size (a later, smaller plan would otherwise
+    // lower it under an earlier plan's launches)
+    WH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes));
     // persistent grid: as many CTAs (pairs) as can be co-resident -- with clusters of 2 not
     // every SM necessarily has a partner in its GPC, and a CTA pair that does not fit would
     // run its whole unit sequence as a second wave
@@ -2162,7 +2260,7 @@ static int umma_prepare_impl(Plan &p) {
 }
 
 int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
-                uint32_t *arrive, uint32_t *abandon) {
+                uint32_t *arrive, uint32_t *abandon, uint32_t *nfbad, uint32_t *nfctl) {
     UmmaArgs a{};
     a.x = x; a.ld_x = ld_x; a.N = p.N; a.F = p.F; a.hop = p.hop;
     a.row_tiles = p.row_tiles; a.V = p.V; a.P = p.P; a.Cc = p.Cc; a.panels = p.panels; a.rs = p.rs;
@@ -2190,6 +2288,8 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.abandon = a.arrive ? abandon : nullptr;
     a.ab_words = p.ab_words;
     a.force_fixup = p.force_fixup ? 1 : 0;
+    a.nfbad = nfbad; a.nfctl = nfctl;
+    a.scales = p.d_scales; a.half = p.d_half; a.Cw = p.C; a.Bw = p.B;
     a.clips = clips;
     a.ring_bytes = (uint32_t)p.ring_bytes;
     a.win_half_bytes = (uint32_t)p.panels * (uint32_t)p.win_rows * 128u;

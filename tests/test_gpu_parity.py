@@ -535,3 +535,21 @@ def test_long_signal_and_empty_batch():
     plan = wh.CwthPlan(sc, None, 64, 1000, max_clips=2)
     empty = plan.execute(torch.empty((0, 1000), dtype=torch.float32, device="cuda"))
     assert tuple(empty.shape) == (0, 4, 16)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_plans_sharing_a_kernel_keep_their_shared_memory(engine):
+    """A plan created after another one with the same kernel instantiation but a smaller
+    shared-memory footprint must not break the earlier plan's launches (the kernel's dynamic
+    smem attribute is per function, not per plan)."""
+    x = synth.make_batch(2, clips=2, n=20000)
+    big = wh.CwthPlan(np.geomspace(1, 128, 16), None, 64, 20000, wavelet="rmor", output="abs", engine=engine,
+                     max_clips=2)
+    small = wh.CwthPlan(np.geomspace(1, 8, 16), None, 64, 20000, wavelet="rmor", output="abs", engine=engine,
+                       max_clips=2)
+    a = small.execute_host(x)
+    b = big.execute_host(x)
+    ref = O.cwth_batch(x, np.geomspace(1, 128, 16), 64, wavelet="rmor", output="abs")
+    assert row_rel_err(b, ref) <= ROW_TOL and np.isfinite(a).all()
+    big.close()
+    small.close()

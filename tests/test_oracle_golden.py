@@ -162,3 +162,26 @@ def test_oracle_errors():
         O.cwth_batch(np.zeros(10, np.float32), [1.0], 0)
     with pytest.raises(ValueError):
         O.cwth_batch(np.zeros(10, np.float32), [0.0], 1)
+
+
+def test_nonfinite_fixture_follows_the_support_rule():
+    """tests/golden/nonfinite.npz (the reference's outputs on NaN / inf inputs): the non-finite
+    coefficients are exactly those whose support holds a non-finite sample."""
+    import math
+    import os
+
+    from conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "nonfinite.npz"))
+    names = sorted({k.split("__")[0] for k in g.files})
+    assert len(names) == 6
+    for n in names:
+        x, sc, hop, ref = g[f"{n}__x"], g[f"{n}__scales"], int(g[f"{n}__hop"]), g[f"{n}__ref"]
+        bad = np.where(~np.isfinite(x))[0]
+        k = np.arange(ref.shape[1])
+        for s, a in enumerate(sc):
+            L = math.ceil(6.0 * a * math.sqrt(0.75))
+            exp = np.zeros(ref.shape[1], bool)
+            for t in bad:
+                exp |= np.abs(k * hop - t) <= L
+            np.testing.assert_array_equal(~np.isfinite(ref[s]), exp)
