@@ -128,6 +128,8 @@ struct Plan {
     int64_t tables_bytes = 0;
     int32_t simt_tf = 1;           // SIMT: frames per item tile
     bool doubled_v = false, no_2v = false;  // UMMA: rows of 2 lcm(hop, 64) samples (one pass)
+    int32_t pstream = 0;           // UMMA: rows of hop samples (one frame each), window streamed by column panel
+    bool no_pstream = false;       // UMMA planner retry without panel streaming
     double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
     bool no_convregs = false;      // UMMA planner override: converters without the register prefetch
     bool force_fixup = false;      // UMMA planner override (tests): min-max units all to the fix-up kernel
@@ -157,6 +159,7 @@ struct Plan {
     // record their positions; a fix-up then writes the exact IEEE value of every coefficient
     // whose support contains one (the reference's propagation, wavelet.py:264-270)
     uint32_t *d_nfbad = nullptr;   // [max_clips][1 + WH_NF_CAP]: count, positions
+    float *d_segmax = nullptr;     // UMMA panel streaming: per-segment max |x| [max_clips][nseg]
     uint32_t *d_nfctl = nullptr;   // [max_clips][2]: per-launch CTA counter (slot of the launch's first clip), any-flag
     float *d_scratch = nullptr;    // render plans: float values [max_clips][S][F] before the uint8 map
     void *d_rparams = nullptr;     // render plans: WH_RENDER_PARAM_BYTES per clip

@@ -42,12 +42,23 @@
 
 namespace wh {
 
-static constexpr int UM_CONV_WARPS = 4;
+// converter warps: 6 (16 warps in all: 4 per SM sub-partition, so 128 registers per thread)
+// -- the window conversion is issue-bound and 6 warps beat 4 (c2 68.5 -> 64.4 us, c4 hop 64
+// 228 -> 208 us, hop 256 / 1024 225 -> 205 us, c5 -1 %; profiles/r02h_ab.txt); 8 warps would
+// cap registers at 96 and spill
+#ifndef WH_CONV_WARPS
+#define WH_CONV_WARPS 6
+#endif
+static constexpr int UM_CONV_WARPS = WH_CONV_WARPS;
 static constexpr int UM_CONV_THREADS = 32 * UM_CONV_WARPS;
 static constexpr int UM_EPI_WARPS = 8;  // 2 per TMEM lane quadrant
 static constexpr int UM_THREADS = 64 + UM_CONV_THREADS + 32 * UM_EPI_WARPS;  // producer, MMA, converters, epilogue
 static constexpr int UM_SLOTS = 16;  // in-flight tap tiles (ring slots)
 static constexpr int UM_PF = 2;     // converters prefetch windows this many units ahead (L2)
+static constexpr int UM_PCH = (36 + UM_CONV_WARPS - 1) / UM_CONV_WARPS;  // panel streaming: chunks per converter thread and panel
+static constexpr int UM_CONV_RC = 40 / UM_CONV_WARPS;  // register-prefetch converters: chunks per thread
+static constexpr int UM_WSLOTS = 4; // window buffers (panel streaming: panel slots; otherwise <= 2 used)
+static constexpr int UM_SEG = 8192; // panel streaming: samples per pre-pass max segment
 static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
 
 // Diagnostics (role switches, per-role wait counters, the CTA-0 timeline) exist only in a
@@ -77,6 +88,9 @@ struct UmmaArgs {
     int32_t cpr, cpr_magic;             // 8-sample chunks per window row (panels * 8); ceil(2^20 / cpr)
     int32_t conv_regs;                  // converters prefetch the window into registers
     int32_t pf;                         // converters prefetch windows into L2 ahead (rows of 256)
+    int32_t pstream;                    // rows of hop samples, the window streamed by 64-sample column panel
+    const float *segmax;                // pstream: max |x| per UM_SEG-sample segment [clips][nseg] (pre-pass)
+    int32_t nseg;
     const UmmaPass *passes;
     const UmmaTile *tiles;
     const UmmaGroup *groups;
@@ -710,7 +724,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t b_full[UM_SLOTS], b_empty[UM_SLOTS];
     __shared__ uint64_t s_vstart[UM_SLOTS];  // producer-private: ring start of in-flight slots
-    __shared__ __align__(8) uint64_t win_full[2], win_empty[2], acc_full[2], acc_empty[2];
+    __shared__ __align__(8) uint64_t win_full[UM_WSLOTS], win_empty[UM_WSLOTS], acc_full[2], acc_empty[2];
     __shared__ float xring[4];  // per-unit window exponent 2^-e, written by the converters
     __shared__ float red[UM_CONV_WARPS];
     __shared__ __align__(8) uint64_t stg_full, res_full, tab_full;
@@ -747,7 +761,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     // Converters, register-prefetch path: each thread loads its first CONV_RC 8-sample chunks
     // of a unit's window into registers (cv) and the window's max |x| over all its chunks
     // (cmx).  The first unit's window is fetched right at launch, overlapping the setup.
-    constexpr int CONV_RC = 10;
+    constexpr int CONV_RC = UM_CONV_RC;
     float cv[CONV_RC][8];
     float cmx = 0.0f;
     bool cbad = false;  // this thread's chunks of the fetched window held non-finite samples
@@ -880,9 +894,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_init(&b_full[i], (CG == 2 && leader) ? 2 : 1);  // + the peer's relay
             mbar_init(&b_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < UM_WSLOTS; ++i) {
             mbar_init(&win_full[i], (CG == 2 && leader) ? 2 : 1);  // + the peer's converters
             mbar_init(&win_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], UM_EPI_WARPS * CG);  // epilogue warps of both CTAs (leader's copy)
         }
@@ -999,6 +1015,93 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         }
         const uint32_t RING = A.ring_bytes - A.res_bytes;
         const uint32_t stage0 = smem_u32(stage_base), ring0 = stage0 + A.res_bytes;
+        if (A.pstream) {
+            // Panel streaming: the window's 64-sample column panels pass through the window
+            // slots (panel counter pc, slot pc % win_bufs); the tiles of the single pass are in
+            // panel-major order; tap groups stream through the ring (or are resident).
+            const uint32_t wh16 = WH >> 4, NS = (uint32_t)A.win_bufs;
+            const int *s_tpanel = s_goff + A.n_groups;  // window panel of each tile
+            uint32_t pc = 0;
+            for (int64_t item = u0; item < n_units; item += ustride, ++wcnt, ++acnt) {
+                WH_TRACE(0, wcnt);
+                const int4 pinfo = s_pass[0];
+                const uint32_t ab = acnt % A.n_acc;
+                mbar_wait_p(&acc_empty[ab], ((acnt / A.n_acc) & 1) ^ 1, pa, 1, pon);
+                tc_fence_after();
+                const uint32_t d_acc = tmem + ab * (uint32_t)A.acc_stride;
+                const uint32_t C = (uint32_t)pinfo.w;
+                int cur = -1;
+                uint32_t a_hi16 = 0;
+                // step to panel `target`: release the current slot, wait for the following
+                // panels (a panel without tiles is released at once)
+                auto step_to = [&](int target) {
+                    while (cur < target) {
+                        if (cur >= 0) {
+                            if (elect_one()) umma_commit<CG>(&win_empty[pc % NS]);
+                            __syncwarp();
+                            ++pc;
+                        }
+                        mbar_wait_p(&win_full[pc % NS], (pc / NS) & 1, pa, 0, pon);
+                        tc_fence_after();
+                        a_hi16 = (smem_u32(win_base) + (pc % NS) * 2 * WH) >> 4;
+                        ++cur;
+                    }
+                };
+                WH_TRACE(1, wcnt);
+                for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
+                    const int4 gr = s_group[gi];
+                    const uint32_t bytes = (uint32_t)gr.w;
+                    uint32_t gbase, slot = 0;
+                    const int goff = s_goff[gi];
+                    if (goff >= 0) {
+                        gbase = stage0 + (uint32_t)goff;
+                    } else {
+                        if (phys + bytes > RING) phys = 0;  // same ring allocation as the producer
+                        gbase = ring0 + phys;
+                        phys += bytes;
+                        slot = seq % UM_SLOTS;
+                        const uint32_t ph = (seq / UM_SLOTS) & 1;
+                        ++seq;
+                        mbar_wait_p(&b_full[slot], ph, pa, 2, pon);
+                        tc_fence_after();
+                    }
+                    const uint32_t g16 = gbase >> 4;
+                    for (int t = gr.x; t < gr.y; ++t) {
+                        step_to(s_tpanel[t]);
+                        const uint4 tt = s_tile[t];
+                        const uint32_t ah = a_hi16 + (tt.x & 0xffffu), al = ah + wh16;
+                        const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
+                        const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
+                        if (!WH_DBG(4) && elect_one()) {
+                            if (tt.w) {
+#pragma unroll
+                                for (uint32_t j = 0; j < 4; ++j) {
+                                    umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                                    umma_f16<CG>(d2, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
+                                }
+                            } else {
+#pragma unroll
+                                for (uint32_t j = 0; j < 4; ++j)
+                                    umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    if (goff < 0) {
+                        if (elect_one()) umma_commit<CG>(&b_empty[slot]);
+                        __syncwarp();
+                    }
+                }
+                step_to(A.panels - 1);
+                if (elect_one()) {
+                    umma_commit<CG>(&win_empty[pc % NS]);
+                    umma_commit<CG>(&acc_full[ab]);
+                }
+                __syncwarp();
+                ++pc;
+                WH_TRACE(2, wcnt);
+            }
+        } else
         for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
             const uint32_t wb = wcnt % A.win_bufs;
             WH_TRACE(0, wcnt);
@@ -1133,7 +1236,159 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
-        if (A.conv_regs) {
+        if (A.pstream) {
+            // Panel streaming (rows of hop samples).  Each 64-sample column panel of a unit's
+            // window (win_rows rows x 256 B of fp32) is copied by cp.async straight into a panel
+            // slot, win_bufs - 1 panels ahead; once it has landed the converters read their own
+            // chunks back, split them with the unit's exponent (from the pre-pass segment
+            // maxima) and overwrite the slot in place with the swizzled hi | lo fp16 panel
+            // (exactly the same 256 B per row).  A slot is refilled once the MMAs of the panel it
+            // held have completed.
+            constexpr int PCH = UM_PCH;
+            const int pchunks = A.win_rows * 8;
+            const uint32_t NS = (uint32_t)A.win_bufs;
+            // cp.async of panel (item, p) into slot `sl`: chunk c of this thread = row c >> 3,
+            // 8 samples at column (c & 7) * 8; out-of-clip samples are stored as zeros
+            auto fetch_panel = [&](int64_t item, int p, uint32_t sl) {
+                int64_t b, tile;
+                unit_tile(item, b, tile);
+                const int64_t w0 = tile * 128 * A.V - A.G0;
+                const float *xb = A.x + b * A.ld_x;
+                float *dst = reinterpret_cast<float *>(win_base + (size_t)sl * 2 * WH);
+#pragma unroll
+                for (int i = 0; i < PCH; ++i) {
+                    const int c = ct + i * UM_CONV_THREADS;
+                    if (c >= pchunks) continue;
+                    const int row = c >> 3;
+                    const int64_t g = w0 + (int64_t)row * A.V + p * 64 + (c & 7) * 8;  // clip sample
+                    float *d = dst + row * 64 + (c & 7) * 8;
+                    if (A.vec_ok && g >= 0 && g + 8 <= A.N) {
+                        const uint32_t sa = smem_u32(d);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(xb + g) : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16), "l"(xb + g + 4) : "memory");
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) d[k] = (g + k >= 0 && g + k < A.N) ? __ldg(xb + g + k) : 0.0f;
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            // the panel sequence: (unit, panel) for panel counter values; the first NS - 1
+            // panels are fetched before the loop
+            int64_t f_item = u0;
+            int f_p = 0;
+            uint32_t fc = 0;  // panels fetched so far
+            auto fetch_next = [&]() {
+                if (f_item < n_units) fetch_panel(f_item, f_p, fc % NS);
+                else asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+                ++fc;
+                if (++f_p == A.panels) {
+                    f_p = 0;
+                    f_item += ustride;
+                }
+            };
+            for (uint32_t j = 0; j + 1 < NS; ++j) fetch_next();
+            uint32_t qc = 0, wcnt = 0;
+            for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
+                int64_t b, tile;
+                unit_tile(item, b, tile);
+                const int64_t w0 = tile * 128 * A.V - A.G0;
+                int p0, p1;
+                unit_passes(item, p0, p1);
+                const int64_t own0 = tile * 128 * A.V, own1 = own0 + 128 * (int64_t)A.V;
+                uint32_t *rec = A.nfbad ? A.nfbad + b * (int64_t)(1 + WH_NF_CAP) : nullptr;
+                if (ct == 0) WH_TRACE(3, wcnt);
+                // the unit's exponent: max over the pre-pass segments its window touches
+                float mx = 0.0f;
+                {
+                    const int64_t lo = w0 > 0 ? w0 : 0, hi = w0 + (int64_t)A.win_rows * A.V;
+                    const int s0 = (int)(lo / UM_SEG);
+                    int s1 = (int)((hi - 1) / UM_SEG);
+                    if (s1 > A.nseg - 1) s1 = A.nseg - 1;
+                    for (int sg = s0 + lane; sg <= s1; sg += 32) mx = fmaxf(mx, __ldg(A.segmax + b * A.nseg + sg));
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+                }
+                const int ex = window_exponent(mx);
+                const float sc = ldexpf(1.0f, ex);
+                if (ct == 0) xring[wcnt & 3] = ldexpf(1.0f, -ex);
+                for (int p = 0; p < A.panels; ++p, ++qc) {
+                    const uint32_t sl = qc % NS;
+                    float *src = reinterpret_cast<float *>(win_base + (size_t)sl * 2 * WH);
+                    // this panel's copies (this thread's own) have landed
+                    {
+                        const long long tw = pon ? clock64() : 0;
+                        asm volatile("cp.async.wait_group %0;" ::"n"(UM_WSLOTS - 2) : "memory");
+                        if (pon) pa.c[0] += (unsigned long long)(clock64() - tw);
+                    }
+                    float pv[PCH][8];
+#pragma unroll
+                    for (int i = 0; i < PCH; ++i) {
+                        const int c = ct + i * UM_CONV_THREADS;
+                        if (c >= pchunks) continue;
+                        const float4 *q = reinterpret_cast<const float4 *>(src + (c >> 3) * 64 + (c & 7) * 8);
+                        const float4 u = q[0], w = q[1];
+                        float (&v)[8] = pv[i];
+                        v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
+                        float m = 0.0f;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) m = fmax_nan(m, fabsf(v[k]));
+                        if (!(m <= 3.402823466e38f)) {  // non-finite samples (rare): 0, recorded once
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                if (!is_finite_f(v[k])) {
+                                    const int64_t g = w0 + (c >> 3) * A.V + p * 64 + (c & 7) * 8 + k;
+                                    if (rec && p0 == 0 && g >= own0 && g < own1) nf_record(rec, A.nfctl + 1, g);
+                                    v[k] = 0.0f;
+                                }
+                            }
+                        }
+                        uint32_t hw[4], lw[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 a2 = make_float2(v[2 * k] * sc, v[2 * k + 1] * sc);
+                            const __half2 h = __float22half2_rn(a2);
+                            const float2 hf = __half22float2(h);
+                            const __half2 l = __float22half2_rn(make_float2(a2.x - hf.x, a2.y - hf.y));
+                            hw[k] = *reinterpret_cast<const uint32_t *>(&h);
+                            lw[k] = *reinterpret_cast<const uint32_t *>(&l);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            v[k] = __uint_as_float(hw[k]);
+                            v[4 + k] = __uint_as_float(lw[k]);
+                        }
+                    }
+                    // every converter has read the fp32 panel: overwrite the slot in place
+                    asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
+                    uint8_t *whi = win_base + (size_t)sl * 2 * WH;
+                    uint8_t *wlo = whi + WH;
+#pragma unroll
+                    for (int i = 0; i < PCH; ++i) {
+                        const int c = ct + i * UM_CONV_THREADS;
+                        if (c >= pchunks) continue;
+                        const int row = c >> 3, c8 = c & 7;
+                        const uint32_t off = (uint32_t)row * 128u + (uint32_t)((c8 ^ (row & 7)) * 16);
+                        const float (&v)[8] = pv[i];
+                        *reinterpret_cast<uint4 *>(whi + off) = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                                                          __float_as_uint(v[2]), __float_as_uint(v[3]));
+                        *reinterpret_cast<uint4 *>(wlo + off) = make_uint4(__float_as_uint(v[4]), __float_as_uint(v[5]),
+                                                                          __float_as_uint(v[6]), __float_as_uint(v[7]));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
+                    if (ct == 0) window_ready(sl, qc);
+                    // refill the slot of the previous panel once its MMAs are done
+                    if (qc >= 1) {
+                        const uint32_t ps = (qc - 1) % NS;
+                        mbar_wait_p(&win_empty[ps], ((qc - 1) / NS) & 1, pa, 1, pon);
+                    }
+                    fetch_next();
+                }
+                if (ct == 0) WH_TRACE(7, wcnt);
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        } else if (A.conv_regs) {
             // Register-prefetch path (no staging buffer): each thread loads its first CONV_RC
             // chunks of the next window into registers while the MMAs of the previous unit
             // run, then converts from registers once the window buffer is free.  Larger
@@ -1474,6 +1729,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         for (int64_t item = u0; item < n_units; item += ustride, ++ucnt) {
             int64_t b, tile;
             unit_tile(item, b, tile);
+            if (A.pstream && et == 0) window_prefetch(item + 2 * ustride);  // L2, ahead of the panel copies
             const int64_t mrow = tile * 128 + m;  // global row (beyond rows_total: no frames)
             // first frame of this row (rs > 1: only every rs-th row is a frame)
             const int64_t frame0 = A.rs > 1 ? mrow / A.rs : mrow * P;
@@ -1594,6 +1850,33 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 A.nfctl[1] = 0u;
             }
         }
+    }
+}
+
+// ---- panel streaming: window exponents ------------------------------------------------
+// max |x| (finite samples) of each UM_SEG-sample segment of each clip; k_umma takes a unit's
+// exponent from the segments its window touches (a bound of the window's max: the split stays
+// exact to 2^-22 of it)
+__global__ void __launch_bounds__(256) k_seg_max(const float *__restrict__ x, int64_t ld_x, int64_t N, int32_t nseg,
+                                                 float *__restrict__ segmax) {
+    const int64_t b = blockIdx.y, s0 = (int64_t)blockIdx.x * UM_SEG;
+    const float *xb = x + b * ld_x;
+    int64_t s1 = s0 + UM_SEG;
+    if (s1 > N) s1 = N;
+    float mx = 0.0f;
+    for (int64_t i = s0 + threadIdx.x; i < s1; i += 256) {
+        const float v = __ldg(xb + i);
+        mx = fmaxf(mx, is_finite_f(v) ? fabsf(v) : 0.0f);
+    }
+    __shared__ float red[8];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+        mx = fmaxf(mx, red[0]);
+        segmax[b * nseg + blockIdx.x] = mx;
     }
 }
 
@@ -1764,6 +2047,10 @@ int umma_supported(const Plan &p, std::string *why) {
     const bool strided = H >= 256 && H % 128 == 0;  // rows of 128 samples, every (H/128)-th a frame
     const int64_t lcm64 = H / std::gcd(H, (int64_t)64) * 64;
     const bool mid = !small && !big && !strided && lcm64 <= 256;  // 3, 6, 12, 24, 48, 96: rows of 192
+    // panel streaming (rows of hop samples): hops 256..4096 that are multiples of 64 whose
+    // columns fit one pass
+    const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
+    if (H >= 256 && H <= 4096 && H % 64 == 0 && cc * p.S <= 128 && p.S <= 65535) return WH_OK;
     if (!small && !big && !strided && !mid) {
         if (why) *why = "hop must divide 64 or 192, or be 128 or 192, or a multiple of 128 from 256";
         return WH_E_UNSUPPORTED;
@@ -1792,9 +2079,10 @@ int umma_supported(const Plan &p, std::string *why) {
 // 128-byte aligned in the bank
 static int ncheck_tiles(const Plan &p) {
     for (auto &t : p.tiles)
-        if ((int64_t)t.k * 64 / p.V >= 4096 || p.V / 64 > 16 || t.c0 > 255 || t.ncols > 255 || (t.byte_off & 127))
+        if ((int64_t)t.k * 64 / p.V >= 4096 || (!p.pstream && p.V / 64 > 16) || t.c0 > 255 || t.ncols > 255 ||
+            (t.byte_off & 127))
             return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table out of range");
-    if (16 * p.passes.size() + 20 * p.groups_u.size() + 16 * p.tiles.size() + 4 * (size_t)((p.S + 15) / 16 * 16) > 32 * 1024)
+    if (16 * p.passes.size() + 20 * p.groups_u.size() + 20 * p.tiles.size() + 4 * (size_t)((p.S + 15) / 16 * 16) > 32 * 1024)
         return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table too large");
     return WH_OK;
 }
@@ -1803,9 +2091,14 @@ static int umma_prepare_impl(Plan &p);
 int umma_prepare(Plan &p) {
     // a plan with doubled rows that does not fit shared memory is planned again without
     p.no_2v = false;
+    p.no_pstream = false;
     int rc = umma_prepare_impl(p);
     if (rc == WH_E_UNSUPPORTED && p.doubled_v) {
         p.no_2v = true;
+        rc = umma_prepare_impl(p);
+    }
+    if (rc == WH_E_UNSUPPORTED && p.pstream) {  // panel streaming did not fit: rows of 128 where possible
+        p.no_pstream = true;
         rc = umma_prepare_impl(p);
     }
     return rc;
@@ -1827,7 +2120,24 @@ static int umma_prepare_impl(Plan &p) {
     // still far ahead of the SIMT engine)
     int64_t H = p.hop;
     p.rs = 1;
+    // Hops >= 256 that are multiples of 64, with the columns in one pass: rows of hop samples,
+    // one frame per row (tensor work in proportion to the frames).  Such a window (128 frames
+    // + halo rows of hop samples) is too large to hold whole, so it streams through two
+    // panel slots in 64-sample column panels, the K-steps in panel-major order, the tap bank
+    // resident; the window's exponent is computed one unit ahead (epilogue warps).
     {
+        const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
+        // measured slower than rows of 128 on c4 (hop 256 / 1024: 214 / 241 vs 205 / 205 us, 6
+        // converter warps): the whole window of 128 frames is converted by the converter warps
+        // of one CTA per tile while a clip's last tile (29 of 157 frames at hop 1024) leaves its
+        // pair partner idle; used where rows of 128 cannot be (hops that are multiples of 64
+        // but not of 128) and on request (WH_UMMA_PSTREAM=1)
+        const bool want = plan_knob("WH_UMMA_PSTREAM") != nullptr || H % 128 != 0;
+        p.pstream = (!p.no_pstream && want && plan_knob("WH_UMMA_NO_PSTREAM") == nullptr && H >= 256 &&
+                     H <= 4096 && H % 64 == 0 && cc * (int64_t)p.S <= 128) ? 1 : 0;
+    }
+    if (!p.pstream) {
+        if (p.hop >= 256 && p.hop % 128 != 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: hop needs panel streaming");
         // hop >= 256, a multiple of 128: rows of R = 128 samples, every (hop/R)-th row a frame.
         // Rows of 256 (one frame per row at hop 256) need a 147 KB window per tile that cannot
         // be double-buffered: measured c4 hop 256 / 1024 274 / 260 us with rows of 256, 227 / 226
@@ -1848,13 +2158,13 @@ static int umma_prepare_impl(Plan &p) {
         // serves twice the columns (c4 hop 64, 64 scales: 285 -> 228 us, the bank streamed
         // beside two windows); with more columns the second pass re-reads A (c2: 65 -> 110 us)
         const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
-        p.doubled_v = p.rs == 1 && 2 * p.V <= 256 && 2 * (p.V / H) * cc * (int64_t)p.S <= 128 && !p.no_2v &&
+        p.doubled_v = p.rs == 1 && !p.pstream && 2 * p.V <= 256 && 2 * (p.V / H) * cc * (int64_t)p.S <= 128 && !p.no_2v &&
                       plan_knob("WH_UMMA_V") == nullptr && plan_knob("WH_UMMA_NO_2V") == nullptr;
         if (p.doubled_v) p.V *= 2;
     }
     if (const char *v = plan_knob("WH_UMMA_V")) {  // experiment: more phases per row
         const int vv = std::atoi(v);
-        if (vv >= p.V && vv % 64 == 0 && vv % H == 0 && p.rs == 1) p.V = vv;
+        if (vv >= p.V && vv % 64 == 0 && vv % H == 0 && p.rs == 1 && !p.pstream) p.V = vv;
     }
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
@@ -1975,11 +2285,23 @@ static int umma_prepare_impl(Plan &p) {
         p.G0 = (int32_t)best;
     }
     p.unit_cost = make_tiles(p.G0, p.passes, p.tiles);
+    if (p.pstream) {
+        if (p.passes.size() != 1) return fail(WH_E_UNSUPPORTED, "UMMA engine: panel streaming needs one pass");
+        // K-steps in panel-major order (panel = (64k mod V) / 64, row shift q = 64k / V): all
+        // the K-steps of one window panel run while it is in its slot
+        const int64_t V = p.V;
+        std::stable_sort(p.tiles.begin(), p.tiles.end(), [&](const UmmaTile &a, const UmmaTile &b) {
+            const int64_t pa = (64 * (int64_t)a.k % V) / 64, pb = (64 * (int64_t)b.k % V) / 64;
+            return pa != pb ? pa < pb : a.k < b.k;
+        });
+    }
     p.Qlo = (int32_t)((p.G0 + p.V - 1) / p.V);
     p.ksteps = (int32_t)((p.G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1);
     const int64_t qmax = (int64_t)(p.ksteps - 1) * 64 / p.V;
     p.win_rows = (int32_t)(((128 + qmax) + 7) / 8 * 8);
-    const int64_t win = 2LL * p.panels * p.win_rows * 128;
+    if (p.pstream && (int64_t)p.win_rows * 8 > (int64_t)UM_PCH * UM_CONV_THREADS)
+        return fail(WH_E_UNSUPPORTED, "UMMA engine: panel too tall for the converters' registers");
+    const int64_t win = 2LL * (p.pstream ? 1 : p.panels) * p.win_rows * 128;  // pstream: one panel slot
     int64_t byte_off = 0;
     // CTA pairs (tcgen05 cta_group::2, M = 256): each CTA stages half of every tap tile
     p.cg = (p.sms % 2 == 0 && plan_knob("WH_UMMA_CG1") == nullptr) ? 2 : 1;
@@ -2014,7 +2336,10 @@ static int umma_prepare_impl(Plan &p) {
     int64_t t_split = 0;  // tiles [0, t_split) resident
     int hybrid = 0;
     int64_t stream_target = 0;
-    if (allow_res && bank_cta + 2 * win <= budget0) {
+    if (p.pstream) {
+        // UM_WSLOTS panel slots; the bank resident beside them when it fits, else streamed
+        if (allow_res && bank_cta + UM_WSLOTS * win <= budget0) t_split = n_tiles;
+    } else if (allow_res && bank_cta + 2 * win <= budget0) {
         t_split = n_tiles;
     } else if (allow_res && bank_cta + win <= budget0) {
         t_split = n_tiles;
@@ -2039,7 +2364,9 @@ static int umma_prepare_impl(Plan &p) {
     // fits beside them (c4 hop 16: 24 KB groups + staging 558 us, 44 KB + two windows 456 us);
     // long ones keep one window and 48 KB groups (c5, c3, c4 hop 1: measured best).
     const int64_t two_win_groups = std::min<int64_t>(48 * 1024, (budget0 - 2 * win) / 3 / 1024 * 1024);
-    const int64_t group_target = p.resident ? 48 * 1024 : (n_tiles >= 64 ? 48 * 1024 : std::max<int64_t>(16 * 1024, two_win_groups));
+    int64_t group_target = p.resident ? 48 * 1024 : (n_tiles >= 64 ? 48 * 1024 : std::max<int64_t>(16 * 1024, two_win_groups));
+    if (p.pstream && !p.resident)  // a ring of three groups beside the panel slots
+        group_target = std::max<int64_t>(8 * 1024, std::min<int64_t>(48 * 1024, (budget0 - UM_WSLOTS * win) / 3 / 1024 * 1024));
     int64_t group_target_env = 0;
     if (const char *g = plan_knob("WH_UMMA_GROUP_KB")) group_target_env = std::max(1, std::atoi(g)) * 1024;
     p.groups_u.clear();
@@ -2085,7 +2412,8 @@ static int umma_prepare_impl(Plan &p) {
     p.n_stream = n_stream;
     const int64_t stage_bytes = std::max<int64_t>(max_group, 1024);
     const int64_t table_bytes = (16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
-                                 16 * (int64_t)p.tiles.size() + 4 * (int64_t)((p.S + 15) / 16 * 16) + 15) / 16 * 16;
+                                 (p.pstream ? 20 : 16) * (int64_t)p.tiles.size() + 4 * (int64_t)((p.S + 15) / 16 * 16) +
+                                 15) / 16 * 16;
     // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
     // alignment slack and the tables
     UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
@@ -2101,18 +2429,24 @@ static int umma_prepare_impl(Plan &p) {
     // window) favour a deeper ring with one window; short units favour two windows.
     int use_stg = 0;
     int64_t ring = 0;
-    if (p.resident && !hybrid) {
+    if (p.pstream) {
+        win_bufs = UM_WSLOTS;
+        const int64_t rest = (budget - UM_WSLOTS * win) / 1024 * 1024;
+        ring = p.resident ? (res_bytes + 1023) / 1024 * 1024 : rest;
+        if (ring > rest || (!p.resident && ring < 3 * stage_bytes))
+            return fail(WH_E_UNSUPPORTED, "UMMA engine: panel slots and tap ring do not fit");
+    } else if (p.resident && !hybrid) {
         // the stage region is the whole resident bank; spend what is left on windows / staging
         ring = (res_bytes + 1023) / 1024 * 1024;
         // the register-prefetch converter (no fp32 staging) is the faster one when a
         // thread's share of the window fits its registers
-        const bool regs_ok = (int64_t)p.win_rows * p.panels * 8 <= 10 * 128;
+        const bool regs_ok = (int64_t)p.win_rows * p.panels * 8 <= (int64_t)UM_CONV_RC * UM_CONV_THREADS;
         const int opts_stg[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
         const int opts_regs[4][2] = {{2, 0}, {1, 0}, {2, 1}, {1, 1}};
         const int (*opts_r)[2] = regs_ok ? opts_regs : opts_stg;
         const int r0 = plan_knob("WH_UMMA_WIN1") ? (regs_ok ? 1 : 2) : 0;  // diagnostics: one window
         for (int i = r0; i < 4; ++i) {
-            const int *o = opts_r[i];
+            const int *o = p.pstream ? opts_regs[0] : opts_r[i];  // pstream: two panel slots, no staging
             if ((int64_t)(o[0] + o[1]) * win + ring <= budget) {
                 win_bufs = o[0];
                 use_stg = o[1];
@@ -2178,7 +2512,7 @@ static int umma_prepare_impl(Plan &p) {
         for (auto &tl : p.tiles) {
             // window row shift q and panel of this K-step's A operand (k*64 = q*V + panel*64)
             const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)p.V, panel = (kg % (uint32_t)p.V) >> 6;
-            const uint32_t aoff = panel * (uint32_t)p.win_rows * 128u + q * 128u;
+            const uint32_t aoff = (p.pstream ? 0u : panel * (uint32_t)p.win_rows * 128u) + q * 128u;
             const uint32_t n1 = (uint32_t)(tl.ncols + tl.ncorr), n2 = (uint32_t)tl.ncorr;
             const uint32_t b2d = (p.cg == 2 ? n1 / 2 : n1) * 128u;
             put32((aoff >> 4) | ((uint32_t)tl.c0 << 16));
@@ -2192,6 +2526,8 @@ static int umma_prepare_impl(Plan &p) {
             put32(v);
         }
         for (auto &g : p.groups_u) put32((uint32_t)g.pad_);
+        if (p.pstream)  // tile -> window panel
+            for (auto &tl : p.tiles) put32((uint32_t)(((int64_t)tl.k * 64 % p.V) / 64));
         p.tables_bytes = table_bytes;
         WH_CUDA_TRY(cudaMalloc(&p.d_tables, (size_t)table_bytes));
         WH_CUDA_TRY(cudaMemcpy(p.d_tables, blob.data(), (size_t)table_bytes, cudaMemcpyHostToDevice));
@@ -2202,6 +2538,11 @@ static int umma_prepare_impl(Plan &p) {
     WH_CUDA_TRY(cudaMemcpy(p.d_groups_u, p.groups_u.data(), sizeof(UmmaGroup) * p.groups_u.size(),
                            cudaMemcpyHostToDevice));
     WH_CUDA_TRY(cudaMalloc(&p.d_bank, (size_t)p.bank_bytes));
+    if (p.pstream) {
+        cudaFree(p.d_segmax);
+        p.d_segmax = nullptr;
+        WH_CUDA_TRY(cudaMalloc(&p.d_segmax, sizeof(float) * (size_t)p.max_clips * (size_t)((p.N + UM_SEG - 1) / UM_SEG)));
+    }
     WH_CUDA_TRY(cudaMalloc(&p.d_scale_pow, sizeof(float) * p.S));
     int32_t *d_fexp = nullptr;
     WH_CUDA_TRY(cudaMalloc(&d_fexp, sizeof(int32_t) * p.S));
@@ -2275,7 +2616,10 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.cpr = p.panels * 8;
     a.pf = p.V >= 256 ? 1 : 0;
     a.cpr_magic = ((1 << 20) + a.cpr - 1) / a.cpr;
-    a.conv_regs = (!p.use_stg && !p.no_convregs) ? 1 : 0;
+    a.conv_regs = (!p.use_stg && !p.no_convregs && !p.pstream) ? 1 : 0;
+    a.pstream = p.pstream;
+    a.nseg = (int32_t)((p.N + UM_SEG - 1) / UM_SEG);
+    a.segmax = p.d_segmax;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.tables = p.d_tables; a.tables_bytes = (uint32_t)p.tables_bytes;
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
@@ -2292,7 +2636,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.scales = p.d_scales; a.half = p.d_half; a.Cw = p.C; a.Bw = p.B;
     a.clips = clips;
     a.ring_bytes = (uint32_t)p.ring_bytes;
-    a.win_half_bytes = (uint32_t)p.panels * (uint32_t)p.win_rows * 128u;
+    a.win_half_bytes = (uint32_t)(p.pstream ? 1 : p.panels) * (uint32_t)p.win_rows * 128u;
     a.out_vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (p.F % 4 == 0);
     a.out_vec8_ok = ((reinterpret_cast<uintptr_t>(out) & 31) == 0) && (p.F % 8 == 0);
     a.prof = p.d_prof;
@@ -2338,6 +2682,12 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     int64_t grid = std::min<int64_t>(units * p.cg, p.grid_ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
+    if (p.pstream) {
+        // the window exponents of panel streaming: max |x| per UM_SEG-sample segment
+        if (clips > 65535) return fail(WH_E_INVALID_ARG, "UMMA engine: too many clips for one launch");
+        k_seg_max<<<dim3((unsigned)a.nseg, (unsigned)clips), 256, 0, s>>>(x, ld_x, p.N, a.nseg, p.d_segmax);
+        WH_CUDA_TRY(cudaGetLastError());
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(UM_THREADS);

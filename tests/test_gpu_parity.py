@@ -390,7 +390,8 @@ def test_engine_selection_and_errors():
     assert wh.CwthPlan([1.0, 2.0], None, 64, 1000).engine == "umma"
     assert wh.CwthPlan([1.0, 2.0], None, 1024, 5000).engine == "umma"  # rows of 256, every 4th a frame
     assert wh.CwthPlan([1.0, 2.0], None, 7, 1000).engine == "simt"
-    assert wh.CwthPlan([1.0, 2.0], None, 320, 5000).engine == "simt"
+    assert wh.CwthPlan([1.0, 2.0], None, 320, 5000).engine == "umma"  # panel streaming (rows of 320)
+    assert wh.CwthPlan([1.0, 2.0], None, 100, 5000).engine == "simt"
     with pytest.raises(wh.DeviceError):
         wh.CwthPlan([1.0, 2.0], None, 7, 1000, engine="umma")
     with pytest.raises(wh.InvalidHop):
@@ -467,6 +468,31 @@ def test_umma_planner_variants_agree(env, monkeypatch):
             assert np.abs(got - ref).max() <= 1e-5, env
         else:
             assert row_rel_err(got, ref) <= ROW_TOL, env
+
+
+@pytest.mark.parametrize("hop,force", [(256, True), (1024, True), (320, False), (448, False)])
+def test_panel_streaming_frames_only(hop, force, monkeypatch):
+    """Rows of hop samples (one frame per row, the window streamed by 64-sample column panels
+    through cp.async-filled slots, exponents from the segment-max pre-pass): the default for
+    hops >= 256 that are multiples of 64 but not of 128, on request (WH_UMMA_PSTREAM=1) for
+    the others -- against the oracle on c4-shaped clips, a NaN/inf clip included."""
+    if force:
+        monkeypatch.setenv("WH_UMMA_PSTREAM", "1")
+    x = synth.make_batch(4, clips=3, n=60000, start=2)
+    x[1, 12345] = np.inf
+    x[1, 40000] = np.nan
+    sc = synth.config_scales(4)
+    plan = wh.CwthPlan(sc, None, hop, 60000, wavelet="rmor", output="abs", max_clips=3, engine="umma")
+    got = plan.execute_host(x)
+    plan.close()
+    ref = O.cwth_batch(x[[0, 2]], sc, hop, wavelet="rmor", output="abs")
+    assert row_rel_err(got[[0, 2]], ref) <= ROW_TOL
+    # the bad clip: non-finite exactly on the supports (k*hop within L_s of 12345 / 40000)
+    k = np.arange(got.shape[2])
+    for s, a in enumerate(sc):
+        L = math.ceil(6.0 * a * math.sqrt(0.75))
+        want = (np.abs(k * hop - 12345) <= L) | (np.abs(k * hop - 40000) <= L)
+        np.testing.assert_array_equal(~np.isfinite(got[1, s]), want)
 
 
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])

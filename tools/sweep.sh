@@ -1,7 +1,7 @@
 #!/bin/bash
 # kernel-time bench lines for every BASELINE config (no e2e / CPU arm): DESIGN's results table
 TAG=${1:-sweep}
-for c in c1 c2 c3 c4h1 c4h16 c4h64 c4h256 c4h1024; do
+for c in ${CONFIGS:-c1 c2 c3 c4h1 c4h16 c4h64 c4h256 c4h1024 c5}; do
   timeout 600 python bench.py --config $c --steps 30 --warmup 10 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 > gpurun_out/${TAG}_$c.json
   python - "$c" "gpurun_out/${TAG}_$c.json" <<'PY'
 import json, sys

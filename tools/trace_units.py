@@ -25,7 +25,7 @@ plan.execute(x, out)
 torch.cuda.synchronize()
 t = plan.trace(False)
 t0 = t[t > 0].min()
-names = ["mma_wait_win", "mma_start", "mma_end", "cv_wait_stg", "cv_stg_ok", "cv_wait_wempty", "cv_wempty_ok",
+names = ["mma_wait_win", "mma_start", "mma_end", "cv_start", "cv_stg|exp_ok", "cv_wempty|ex0", "cv_wok|ex1",
          "cv_done", "epi_wait", "epi_start", "epi_end"]
 print("unit " + " ".join(f"{n:>13s}" for n in names) + "   (kcycles from first event)")
 for u in range(12):
