@@ -83,6 +83,12 @@ int build_fold_bank(Plan &p) {
     return WH_OK;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns_api() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---------------------------------------------------------------------------------------
 // Per-clip min-max (scalogram.py:77-83 affine map, without x255/round/uint8).
 __global__ void k_minmax_reset(uint32_t *mm, uint32_t *arrive, uint32_t *abandon, int32_t ab_words, int64_t clips) {
@@ -97,8 +103,9 @@ __global__ void k_minmax_reset(uint32_t *mm, uint32_t *arrive, uint32_t *abandon
     }
 }
 
-__global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip, int vec) {
+__global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip, int vec, const uint32_t *done) {
     int64_t b = blockIdx.y;
+    if (done && done[b] == WH_CLIP_NORMALISED) return;  // the concurrent normaliser did this clip
     float lo = key2f(mm[2 * b]), hi = key2f(mm[2 * b + 1]);
     bool constant = (hi == lo);
     float sc = constant ? 0.0f : 1.0f / (hi - lo);
@@ -118,6 +125,79 @@ __global__ void k_minmax_apply(float *out, const uint32_t *mm, int64_t per_clip,
     for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_clip;
          i += (int64_t)gridDim.x * blockDim.x)
         base[i] = constant ? 0.0f : (base[i] - lo) * sc;
+}
+
+// Concurrent per-clip min-max (mode 2): a few CTAs on SMs of their own, running beside
+// k_umma, normalise each clip as soon as all its units have arrived (arrive[b] reaches
+// `target`; the epilogue's release-add follows its stores and key atomics) -- the clip's
+// raw values were written a round or two earlier and are read back mostly from L2, so the
+// read-modify-write overlaps the tensor-bound kernel instead of following it.  Bounded waits:
+// once one wait times out (k_umma not running beside it), every CTA stops waiting and the
+// rest is left to the trailing masked pass, as are clips with non-finite samples (their
+// values are final only after k_umma's fix-up).  A finished clip is marked
+// WH_CLIP_NORMALISED for that pass.
+__global__ void __launch_bounds__(1024, 1) k_minmax_stream(float *out, const uint32_t *mm, uint32_t *arrive,
+                                                           const uint32_t *nfbad, int64_t per_clip, int64_t clips,
+                                                           uint32_t target, int vec, uint32_t *giveup) {
+    __shared__ int s_go;
+    const int tid = threadIdx.x;
+    for (int64_t b = blockIdx.x; b < clips; b += gridDim.x) {
+        if (tid == 0) {
+            int go = 0;
+            const unsigned long long t0 = globaltimer_ns_api();
+            while (true) {
+                uint32_t c;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(arrive + b) : "memory");
+                if (c >= target) { go = 1; break; }
+                if (*reinterpret_cast<volatile uint32_t *>(giveup)) break;
+                if (globaltimer_ns_api() - t0 > 50000000ull) {  // 50 ms: k_umma is not running beside us
+                    atomicExch(giveup, 1u);
+                    break;
+                }
+                __nanosleep(256);
+            }
+            if (go && nfbad[b * (int64_t)(1 + WH_NF_CAP)] != 0) go = 0;
+            s_go = go;
+        }
+        __syncthreads();
+        const int go = s_go;
+        __syncthreads();
+        if (!go) continue;
+        const float lo = key2f(__ldcg(mm + 2 * b)), hi = key2f(__ldcg(mm + 2 * b + 1));
+        const bool constant = hi == lo;
+        const float sc = constant ? 0.0f : 1.0f / (hi - lo);
+        float *base = out + b * per_clip;
+        const int64_t n4 = vec ? per_clip / 4 : 0;
+        float4 *o = reinterpret_cast<float4 *>(base);
+        constexpr int U = 8;
+        for (int64_t i0 = tid; i0 < n4; i0 += (int64_t)U * 1024) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + (int64_t)u * 1024;
+                if (i < n4) v[u] = __ldcg(o + i);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + (int64_t)u * 1024;
+                if (i >= n4) continue;
+                float4 w = v[u];
+                if (constant) {
+                    w = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+                    w.x = (w.x - lo) * sc; w.y = (w.y - lo) * sc; w.z = (w.z - lo) * sc; w.w = (w.w - lo) * sc;
+                }
+                o[i] = w;
+            }
+        }
+        for (int64_t i = n4 * 4 + tid; i < per_clip; i += 1024)
+            base[i] = constant ? 0.0f : (__ldcg(base + i) - lo) * sc;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            arrive[b] = WH_CLIP_NORMALISED;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -144,12 +224,36 @@ int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, uint32_t *arrive, uint32_
     return WH_OK;
 }
 
-int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s) {
+int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s, const uint32_t *done) {
     int64_t per_clip = (int64_t)p.S * p.F;
     int vec = (per_clip % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
     int64_t work = vec ? per_clip / 4 : per_clip;
     unsigned bx = (unsigned)std::min<int64_t>(std::max<int64_t>((work + 1023) / 1024, 1), 64);
-    k_minmax_apply<<<dim3(bx, (unsigned)clips), 256, 0, s>>>((float *)out, mm, per_clip, vec);
+    k_minmax_apply<<<dim3(bx, (unsigned)clips), 256, 0, s>>>((float *)out, mm, per_clip, vec, done);
+    WH_CUDA_TRY(cudaGetLastError());
+    return WH_OK;
+}
+
+int minmax_stream_launch(Plan &p, int64_t clips, void *out, uint32_t *mm, uint32_t *arrive, const uint32_t *nfbad,
+                         uint32_t target, cudaStream_t s) {
+    const int64_t per_clip = (int64_t)p.S * p.F;
+    const int vec = (per_clip % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    // clusters of 2: the normaliser takes whole SM pairs, so the kernel's CTA pairs still fit
+    // in the rest
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.norm_ctas);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    uint32_t *giveup = arrive + p.max_clips;  // one word after the arrival counters
+    WH_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_minmax_stream, static_cast<float *>(out), static_cast<const uint32_t *>(mm),
+                                   arrive, nfbad, per_clip, clips, target, vec, giveup));
     WH_CUDA_TRY(cudaGetLastError());
     return WH_OK;
 }
@@ -227,6 +331,9 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_minmax); cudaFree(p->d_nfbad); cudaFree(p->d_nfctl); cudaFree(p->d_segmax); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
+    if (p->nstream) cudaStreamDestroy(p->nstream);
+    if (p->nev0) cudaEventDestroy(p->nev0);
+    if (p->nev1) cudaEventDestroy(p->nev1);
     if (p->h_stage) cudaFreeHost(p->h_stage);
     for (int i = 0; i < 2; ++i) {
         if (p->ev_h2d[i]) cudaEventDestroy(p->ev_h2d[i]);
@@ -326,13 +433,19 @@ int wh_plan_create(wh_plan **plan, int device, const double *scales, int32_t n_s
             }
         }
     }
-    if (rc == WH_OK && norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA && !p->minmax_2pass) {
+    if (rc == WH_OK && norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA && p->minmax_mode != 0) {
         // write-once min-max: per-clip unit arrivals + the bitmap of units left to the fix-up
         const int64_t bits = (int64_t)((p->row_tiles + p->cg - 1) / p->cg) * (int64_t)p->passes.size() * p->cg;
         p->ab_words = (int32_t)((bits + 31) / 32);
-        if (cudaMalloc(&p->d_arrive, sizeof(uint32_t) * max_clips) != cudaSuccess ||
+        // (+1 word: the concurrent normaliser's give-up flag)
+        if (cudaMalloc(&p->d_arrive, sizeof(uint32_t) * (max_clips + 1)) != cudaSuccess ||
             cudaMalloc(&p->d_abandon, sizeof(uint32_t) * (size_t)max_clips * p->ab_words) != cudaSuccess)
             rc = fail(WH_E_OOM, "cudaMalloc(min-max arrivals) failed");
+        if (rc == WH_OK && p->minmax_mode == 2 &&
+            (cudaStreamCreateWithFlags(&p->nstream, cudaStreamNonBlocking) != cudaSuccess ||
+             cudaEventCreateWithFlags(&p->nev0, cudaEventDisableTiming) != cudaSuccess ||
+             cudaEventCreateWithFlags(&p->nev1, cudaEventDisableTiming) != cudaSuccess))
+            rc = fail(WH_E_CUDA, "normaliser stream / events failed");
     }
     if (rc == WH_OK && (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
                         cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess))
@@ -382,7 +495,9 @@ int wh_plan_launches(const wh_plan *plan, int64_t clips, int64_t *launches) {
     const int mm = p->norm == WH_NORM_MINMAX ? 2 : 0;
     // + the SIMT engine's non-finite fix-up (the UMMA engine's last CTA does it in-kernel)
     const int nf = p->engine == WH_ENGINE_UMMA ? 0 : 1;
-    *launches = clips > 0 ? (1 + nf + mm + (is_render(*p) ? 3 : 0)) : 0;
+    // + the concurrent normaliser (UMMA min-max mode 2)
+    const int cn = (p->engine == WH_ENGINE_UMMA && p->norm == WH_NORM_MINMAX && p->minmax_mode == 2) ? 1 : 0;
+    *launches = clips > 0 ? (1 + nf + cn + mm + (is_render(*p) ? 3 : 0)) : 0;
     return WH_OK;
 }
 
@@ -438,17 +553,36 @@ static int execute_impl(Plan *p, const float *x_dev, int64_t clips, int64_t ld_x
     void *dst = render ? static_cast<void *>(scratch) : out_dev;
     // the UMMA engine normalises min-max plans inside the kernel (write-once); the SIMT
     // engine keeps the read-modify-write pass
-    const bool inkernel = p->norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA && !p->minmax_2pass;
-    if (p->norm != WH_NORM_NONE) rc = minmax_reset(*p, clips, mm, inkernel ? arrive : nullptr, abandon, s);
+    const bool umma_mm = p->norm == WH_NORM_MINMAX && p->engine == WH_ENGINE_UMMA;
+    const bool inkernel = umma_mm && p->minmax_mode == 1;
+    const bool concurrent = umma_mm && p->minmax_mode == 2;
+    if (p->norm != WH_NORM_NONE)
+        rc = minmax_reset(*p, clips, mm, (inkernel || concurrent) ? arrive : nullptr, abandon, s);
+    if (rc == WH_OK && concurrent) {
+        // the normaliser runs beside the kernel on its own stream and SMs; the caller's stream
+        // waits for it before the trailing masked pass
+        const uint32_t target = (uint32_t)(p->cg * ((p->row_tiles + p->cg - 1) / p->cg) *
+                                           umma_pass_groups(*p, clips));
+        if (cudaMemsetAsync(p->d_arrive + p->max_clips, 0, sizeof(uint32_t), s) != cudaSuccess ||
+            cudaEventRecord(p->nev0, s) != cudaSuccess || cudaStreamWaitEvent(p->nstream, p->nev0, 0) != cudaSuccess)
+            rc = fail(WH_E_CUDA, "normaliser fork failed");
+        if (rc == WH_OK) rc = minmax_stream_launch(*p, clips, out_dev, mm, arrive, nfbad, target, p->nstream);
+        if (rc == WH_OK && cudaEventRecord(p->nev1, p->nstream) != cudaSuccess)
+            rc = fail(WH_E_CUDA, "normaliser event failed");
+    }
     if (rc == WH_OK)
-        rc = (p->engine == WH_ENGINE_UMMA) ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm, inkernel ? arrive : nullptr,
-                                                         abandon, nfbad, nfctl)
-                                           : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm, nfbad, nfctl);
+        rc = (p->engine == WH_ENGINE_UMMA)
+                 ? umma_launch(*p, x_dev, clips, ld_x, dst, s, mm, (inkernel || concurrent) ? arrive : nullptr, abandon,
+                               nfbad, nfctl)
+                 : simt_launch(*p, x_dev, clips, ld_x, dst, s, mm, nfbad, nfctl);
+    if (rc == WH_OK && concurrent && cudaStreamWaitEvent(s, p->nev1, 0) != cudaSuccess)
+        rc = fail(WH_E_CUDA, "normaliser join failed");
     // the SIMT engine's non-finite fix-up is a kernel of its own (the UMMA engine's last CTA
     // does it)
     if (rc == WH_OK && p->engine != WH_ENGINE_UMMA)
         rc = nf_fixup_launch(*p, x_dev, clips, ld_x, dst, p->norm != WH_NORM_NONE ? mm : nullptr, nfbad, s);
-    if (rc == WH_OK && p->norm == WH_NORM_MINMAX && !inkernel) rc = minmax_apply(*p, clips, out_dev, mm, s);
+    if (rc == WH_OK && p->norm == WH_NORM_MINMAX && !inkernel)
+        rc = minmax_apply(*p, clips, out_dev, mm, s, concurrent ? arrive : nullptr);  // mode 2: the clips left
     if (rc == WH_OK && render)
         rc = render_apply(scratch, clips, p->S, p->F, mm, rparams, p->norm == WH_NORM_RENDER_U8 ? 1 : 0,
                           static_cast<uint8_t *>(out_dev), s);

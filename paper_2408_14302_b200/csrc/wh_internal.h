@@ -134,6 +134,13 @@ struct Plan {
     bool no_convregs = false;      // UMMA planner override: converters without the register prefetch
     bool force_fixup = false;      // UMMA planner override (tests): min-max units all to the fix-up kernel
     bool minmax_2pass = false;     // UMMA: per-clip min-max as a separate read-modify-write pass
+    // UMMA per-clip min-max: 0 separate pass after the kernel, 1 in-kernel write-once
+    // (experiment), 2 concurrent normaliser CTAs (k_minmax_stream on its own SMs, fed by the
+    // kernel's per-clip unit arrivals)
+    int32_t minmax_mode = 0;
+    int32_t norm_ctas = 8;         // mode 2: SMs given to the normaliser (clusters of 2)
+    cudaStream_t nstream = nullptr;
+    cudaEvent_t nev0 = nullptr, nev1 = nullptr;
     int32_t pgroups_force = 0;     // UMMA planner override: pass groups per tile pair (0 = modelled)
     int32_t dbg = 0;               // diagnostics role switches (WH_DIAG builds only)
     std::vector<int32_t> fexp;
@@ -189,6 +196,7 @@ int umma_supported(const Plan &p, std::string *why);
 int umma_prepare(Plan &p);
 int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
                 uint32_t *arrive, uint32_t *abandon, uint32_t *nfbad, uint32_t *nfctl);
+int umma_pass_groups(const Plan &p, int64_t clips);
 
 // epilogue helpers (wh_api.cu)
 int minmax_reset(Plan &p, int64_t clips, uint32_t *mm, uint32_t *arrive, uint32_t *abandon, cudaStream_t s);
@@ -196,7 +204,10 @@ constexpr int WH_RENDER_PARAM_BYTES = 24;  // per-matrix affine map of render_ap
 int render_apply(const float *values, int64_t clips, int64_t rows, int64_t cols, const uint32_t *mm, void *params,
                  int32_t flip, uint8_t *out, cudaStream_t s);
 inline bool is_render(const Plan &p) { return p.norm == WH_NORM_RENDER_U8 || p.norm == WH_NORM_RENDER_U8_NOFLIP; }
-int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s);
+int minmax_apply(Plan &p, int64_t clips, void *out, uint32_t *mm, cudaStream_t s, const uint32_t *done = nullptr);
+int minmax_stream_launch(Plan &p, int64_t clips, void *out, uint32_t *mm, uint32_t *arrive, const uint32_t *nfbad,
+                         uint32_t target, cudaStream_t s);
+constexpr uint32_t WH_CLIP_NORMALISED = 0xffffffffu;  // arrive[] value of a clip the normaliser finished
 int nf_fixup_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, uint32_t *mm, uint32_t *bad,
                     cudaStream_t s);
 

@@ -106,6 +106,7 @@ struct UmmaArgs {
     uint32_t *abandon;              // per clip ab_words words: units left to k_minmax_fixup
     int32_t ab_words;               // bit ((tile pair * pgroups + pass group) * CG + CTA rank)
     int32_t force_fixup;            // planner override (tests): every unit goes to the fix-up
+    int32_t arrive_only;            // concurrent normaliser (min-max mode 2): count arrivals, normalise nothing
     uint32_t *nfbad;                // non-finite samples: per clip [1 + WH_NF_CAP] records
     uint32_t *nfctl;                // [0] CTAs done (the last one runs the fix-up), [1] any recorded
     const double *scales;           // for the fix-up's exact taps
@@ -1801,12 +1802,14 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         __threadfence();
                         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.arrive + b) : "memory");
                     }
-                    ++pend;
-                    drain(2);  // at most 2 units behind (a bounded L2 footprint)
+                    if (!A.arrive_only) {
+                        ++pend;
+                        drain(2);  // at most 2 units behind (a bounded L2 footprint)
+                    }
                 }
             }
         }
-        if (A.arrive) drain(0);
+        if (A.arrive && !A.arrive_only) drain(0);
     }
     if (pon && lane == 0) {
         const int role = warp == 0 ? PR_PROD : warp == 1 ? (leader ? PR_MMA : PR_RELAY) : warp < 2 + UM_CONV_WARPS ? PR_CONV : PR_EPI;
@@ -2112,6 +2115,14 @@ static int umma_prepare_impl(Plan &p) {
     // tiles were mostly evicted before the re-read (ncu: 23.3 GB written, 12.1 GB read for
     // 13.1 + 2.6 GB algorithmic) and the re-reads compete with the MMA operand traffic
     p.minmax_2pass = plan_knob("WH_UMMA_MINMAX_INKERNEL") == nullptr;
+    p.minmax_mode = p.minmax_2pass ? 0 : 1;
+    if (const char *m = plan_knob("WH_UMMA_MINMAX")) {  // pass | inkernel | concurrent
+        if (!std::strcmp(m, "pass")) p.minmax_mode = 0;
+        else if (!std::strcmp(m, "inkernel")) p.minmax_mode = 1;
+        else if (!std::strcmp(m, "concurrent")) p.minmax_mode = 2;
+    }
+    p.minmax_2pass = p.minmax_mode != 1;
+    if (const char *n = plan_knob("WH_UMMA_NORM_CTAS")) p.norm_ctas = std::max(2, std::atoi(n) / 2 * 2);
     if (const char *e = plan_knob("WH_UMMA_PGROUPS")) p.pgroups_force = std::atoi(e);
     if (const char *d = diag_knob("WH_UMMA_DBG")) p.dbg = std::atoi(d);
     // hop | 64: rows of 64 samples, P = 64/hop frames (phases) per row; hop = 64..256 (multiple
@@ -2600,6 +2611,45 @@ static int umma_prepare_impl(Plan &p) {
     return WH_OK;
 }
 
+// Pass groups per tile pair for a launch of `clips` clips: split each tile pair's passes into
+// G groups (separate units) when there are too few units to fill the CTA pairs evenly (c3: 80
+// tile pairs on 74 CTA pairs): minimise rounds x unit time, with a unit costing at least one
+// window conversion (~6 k cycles)
+int umma_pass_groups(const Plan &p, int64_t clips) {
+    const int64_t tile_units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
+    const bool concurrent = p.norm == WH_NORM_MINMAX && p.minmax_mode == 2;
+    const int64_t pairs = std::max<int64_t>(1, (p.grid_ctas - (concurrent ? p.norm_ctas : 0)) / p.cg);
+    const int n_passes = (int)p.passes.size();
+    // Among splits within 3 % of the best modelled time, the one whose last round of units is
+    // fullest wins (c3: 11 groups of 3 passes, last round 66 / 74 full: 150 us; 8 groups of 4,
+    // 48 / 74: 165 us; 16 groups of 2, 22 / 74: 163 us -- all model the same 36 pass-rounds).
+    int G = 1;
+    double best = -1.0, best_fill = -1.0;
+    std::vector<std::pair<int, double>> cand;  // (G, modelled time)
+    for (int g = 1; g <= n_passes; ++g) {
+        const int ppu = (n_passes + g - 1) / g;
+        const int gg = (n_passes + ppu - 1) / ppu;  // groups actually formed
+        if (gg != g) continue;
+        const double rounds = std::ceil((double)(tile_units * g) / (double)pairs);
+        const double t = rounds * std::max(p.unit_cost * (double)ppu / n_passes, 6000.0);
+        cand.emplace_back(g, t);
+        if (best < 0 || t < best) best = t;
+    }
+    // (only when there are few tile pairs; otherwise the first split within 3 % of the best)
+    for (auto &c : cand) {
+        if (c.second > best * 1.03) continue;
+        const int64_t rem = (tile_units * c.first) % pairs;
+        const double fill = rem == 0 ? 1.0 : (double)rem / (double)pairs;
+        if (best_fill < 0.0 || (tile_units < 4 * pairs && fill > best_fill + 1e-9)) {
+            G = c.first;
+            best_fill = fill;
+        }
+    }
+    if (p.pgroups_force > 0) G = std::max(1, std::min(n_passes, p.pgroups_force));
+    const int ppu = (n_passes + G - 1) / G;
+    return (n_passes + ppu - 1) / ppu;
+}
+
 int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
                 uint32_t *arrive, uint32_t *abandon, uint32_t *nfbad, uint32_t *nfctl) {
     UmmaArgs a{};
@@ -2632,6 +2682,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.abandon = a.arrive ? abandon : nullptr;
     a.ab_words = p.ab_words;
     a.force_fixup = p.force_fixup ? 1 : 0;
+    a.arrive_only = (a.arrive && p.norm == WH_NORM_MINMAX && p.minmax_mode == 2) ? 1 : 0;
     a.nfbad = nfbad; a.nfctl = nfctl;
     a.scales = p.d_scales; a.half = p.d_half; a.Cw = p.C; a.Bw = p.B;
     a.clips = clips;
@@ -2642,44 +2693,17 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.prof = p.d_prof;
     a.dbg = p.dbg;
     a.trace = p.d_trace;
-    // Split each tile pair's passes into G groups (separate units) when there are too few
-    // units to fill the CTA pairs evenly (c3: 80 tile pairs on 74 CTA pairs): minimise
-    // rounds x unit time, with a unit costing at least one window conversion (~6 k cycles)
     const int64_t tile_units = clips * ((p.row_tiles + p.cg - 1) / p.cg);
-    const int64_t pairs = std::max<int64_t>(1, p.grid_ctas / p.cg);
     const int n_passes = (int)p.passes.size();
-    // Among splits within 3 % of the best modelled time, the one whose last round of units is
-    // fullest wins (c3: 11 groups of 3 passes, last round 66 / 74 full: 150 us; 8 groups of 4,
-    // 48 / 74: 165 us; 16 groups of 2, 22 / 74: 163 us -- all model the same 36 pass-rounds).
-    int G = 1;
-    double best = -1.0, best_fill = -1.0;
-    std::vector<std::pair<int, double>> cand;  // (G, modelled time)
-    for (int g = 1; g <= n_passes; ++g) {
-        const int ppu = (n_passes + g - 1) / g;
-        const int gg = (n_passes + ppu - 1) / ppu;  // groups actually formed
-        if (gg != g) continue;
-        const double rounds = std::ceil((double)(tile_units * g) / (double)pairs);
-        const double t = rounds * std::max(p.unit_cost * (double)ppu / n_passes, 6000.0);
-        cand.emplace_back(g, t);
-        if (best < 0 || t < best) best = t;
-    }
-    // (only when there are few tile pairs; otherwise the first split within 3 % of the best)
-    for (auto &c : cand) {
-        if (c.second > best * 1.03) continue;
-        const int64_t rem = (tile_units * c.first) % pairs;
-        const double fill = rem == 0 ? 1.0 : (double)rem / (double)pairs;
-        if (best_fill < 0.0 || (tile_units < 4 * pairs && fill > best_fill + 1e-9)) {
-            G = c.first;
-            best_fill = fill;
-        }
-    }
-    if (p.pgroups_force > 0) G = std::max(1, std::min(n_passes, p.pgroups_force));
+    const int G = umma_pass_groups(p, clips);
     a.ppu = (n_passes + G - 1) / G;
     a.pgroups = (n_passes + a.ppu - 1) / a.ppu;
     const int64_t units = tile_units * a.pgroups;
     a.arrive_target = (uint32_t)(p.cg * ((p.row_tiles + p.cg - 1) / p.cg) * a.pgroups);
     if (units >= ((int64_t)1 << 31)) return fail(WH_E_INVALID_ARG, "UMMA engine: too many clips for one launch");
-    int64_t grid = std::min<int64_t>(units * p.cg, p.grid_ctas);
+    // min-max mode 2: the concurrent normaliser keeps norm_ctas SMs (pairs) for itself
+    const int64_t ctas = p.grid_ctas - (a.arrive_only ? p.norm_ctas : 0);
+    int64_t grid = std::min<int64_t>(units * p.cg, ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
     if (p.pstream) {

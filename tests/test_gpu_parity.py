@@ -579,3 +579,27 @@ def test_plans_sharing_a_kernel_keep_their_shared_memory(engine):
     assert row_rel_err(b, ref) <= ROW_TOL and np.isfinite(a).all()
     big.close()
     small.close()
+
+
+@pytest.mark.parametrize("mode", ["concurrent", "inkernel"])
+def test_minmax_modes_byte_identical(mode, monkeypatch):
+    """Per-clip min-max computed by the concurrent normaliser CTAs (beside k_umma, fed by the
+    per-clip unit arrivals; WH_UMMA_MINMAX=concurrent) or in-kernel (=inkernel) gives the
+    separate pass's bytes -- the concurrent one also for a clip with a non-finite sample (left
+    to the trailing pass after the fix-up) -- over repeated launches of one plan."""
+    x = synth.make_batch(5, clips=40, n=50000, start=11)
+    if mode == "concurrent":  # (the in-kernel variant does not take non-finite input)
+        x[7, 1234] = np.inf
+    sc = synth.config_scales(5)
+    mk = lambda: wh.CwthPlan(sc, None, 32, 50000, wavelet="cmor", output="abs", norm="minmax",  # noqa: E731
+                             max_clips=40, engine="umma")
+    plan = mk()
+    want = plan.execute_host(x).copy()
+    plan.close()
+    monkeypatch.setenv("WH_UMMA_MINMAX", mode)
+    plan = mk()
+    xd = torch.from_numpy(x).cuda()
+    for _ in range(3):
+        got = plan.execute(xd).cpu().numpy()
+        assert got.tobytes() == want.tobytes()
+    plan.close()
