@@ -284,14 +284,25 @@ class CwthPlan:
             stream = torch.cuda.current_stream(x.device)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         ld_x = x.stride(0) if B > 1 else n  # a size-1 batch dimension may carry stride 0
-        _lib.check(_lib.load().wh_execute(self._h, ctypes.c_void_p(x.data_ptr()), B, ld_x,
-                                          ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(handle)))
+        with self._lock:
+            if not self._h:
+                raise ValueError("plan is closed")
+            _lib.check(_lib.load().wh_execute(self._h, ctypes.c_void_p(x.data_ptr()), B, ld_x,
+                                              ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(handle)))
         return out
 
     def close(self):
-        if getattr(self, "_h", None):
-            _lib.load().wh_plan_destroy(self._h)
-            self._h = None
+        """Release the plan's device memory (waits for a call in flight on another thread).
+        A plan's min-max / render workspace serves one launch at a time: calls on one plan are
+        serialised by its lock, and wh_execute's launches on different streams must not
+        overlap (wh_execute_host orders its own two streams)."""
+        lock = getattr(self, "_lock", None)
+        if lock is None:
+            return
+        with lock:
+            if getattr(self, "_h", None):
+                _lib.load().wh_plan_destroy(self._h)
+                self._h = None
 
     def __del__(self):
         try:
@@ -315,13 +326,14 @@ def get_plan(scales, params, hop, n_samples, *, wavelet, output, norm, clips, de
         if plan is not None and plan.max_clips >= clips:
             _plans.move_to_end(key)
             return plan
-        if plan is not None:
-            plan.close()
+        # a replaced or evicted plan is not closed here: another thread may still hold it (it
+        # got it from this cache); its device memory is released when the last reference goes
+        # (CwthPlan.__del__ -> close, which waits for a running call through the plan's lock)
         plan = CwthPlan(scales, params, hop, n_samples, wavelet=wavelet, output=output, norm=norm,
                         max_clips=max(clips, 1), device=device, engine=engine)
         _plans[key] = plan
         while len(_plans) > _PLAN_CACHE:
-            _plans.popitem(last=False)[1].close()
+            _plans.popitem(last=False)
         return plan
 
 

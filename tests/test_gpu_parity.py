@@ -603,3 +603,19 @@ def test_minmax_modes_byte_identical(mode, monkeypatch):
         got = plan.execute(xd).cpu().numpy()
         assert got.tobytes() == want.tobytes()
     plan.close()
+
+
+def test_cached_plan_survives_eviction():
+    """get_plan's LRU eviction (and replacement by a larger plan) drops the cache's reference
+    only: a caller still holding the plan keeps a working plan (closed when the last reference
+    goes), instead of one freed under it."""
+    from paper_2408_14302_b200.wavelet import get_plan
+
+    x = synth.make_batch(2, clips=1, n=8000)
+    kw = dict(wavelet="rmor", output="abs", norm=None, clips=1, device=0, engine="auto")
+    held = get_plan(np.geomspace(1, 16, 8), None, 16, 8000, **kw)
+    first = held.execute_host(x).copy()
+    for i in range(20):  # more than the cache holds
+        get_plan(np.geomspace(1, 16, 8) * (1 + 0.01 * (i + 1)), None, 16, 8000, **kw)
+    get_plan(np.geomspace(1, 16, 8), None, 16, 8000, **{**kw, "clips": 4})  # replaces the key
+    np.testing.assert_array_equal(held.execute_host(x), first)
