@@ -506,8 +506,15 @@ def run_ours(args, w):
     total_clips = per_rank * world if w["scaling"] == "weak" else (args.clips or w["clips"])
     value = coeffs(w, total_clips) * args.steps / (dev_ms / 1e3)
     if rank == 0:
-        bf16, bf16_sus, hbm, peak_kind = peaks()
+        bf16_burst, bf16_sus, hbm, peak_kind = peaks()
         kern_ms = statistics.median(step_ms)
+        # The tensor peak to compare against: the sustained bf16 figure (matmul back to back
+        # for 4 s, at the power cap) for a kernel that runs inside a long step -- a step of
+        # >= 5 ms keeps the GPU at its power limit as the sustained measurement does (c5:
+        # 28-30 ms, sw_power_cap) -- else the burst figure (a kernel timed alone between L2
+        # flushes)
+        sustained = bool(bf16_sus) and kern_ms >= 5.0
+        bf16 = bf16_sus if sustained else bf16_burst
         flops = alg_flops(w, per_rank)
         exec_flops = plan.mma_flops(per_rank)
         achieved = flops / (kern_ms / 1e3) / 1e12
@@ -539,8 +546,13 @@ def run_ours(args, w):
                                           "algorithmic (minus skipped tail cross terms) + K padding"},
                   "hbm_view": {"achieved_gbs": alg_bytes / kern_s / 1e9, "peak_gbs": hbm,
                                "frac": alg_bytes / kern_s / 1e9 / hbm},
-                  "peak_source": f"{peak_kind} MEASURED_PEAKS.json burst figures (the kernel "
-                                 f"is timed alone between L2 flushes)"}
+                  "peak_source": (f"{peak_kind} MEASURED_PEAKS.json: bf16 "
+                                  f"{'sustained' if sustained else 'burst'} "
+                                  f"({bf16:.1f} TF/s; burst {bf16_burst:.1f}), HBM copy "
+                                  f"bandwidth (burst) -- "
+                                  + ("the kernel runs inside a step of >= 5 ms at the power "
+                                     "limit, as the sustained matmul does" if sustained else
+                                     "the kernel is timed alone between L2 flushes"))}
         if t_hbm >= t_tensor:
             roofline = {"bound": "hbm", "achieved": alg_bytes / kern_s / 1e9, "peak": hbm,
                         "unit": "GB/s", "frac": alg_bytes / kern_s / 1e9 / hbm, **common}
