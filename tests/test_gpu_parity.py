@@ -193,6 +193,25 @@ def test_c4_hop_sweep_parity(hop):
     assert row_rel_err(got, ref) <= ROW_TOL
 
 
+@pytest.mark.parametrize("hop", [16, 64, 256, 1024])
+def test_c4_full_launch_sampled_clips(hop):
+    """The 256-clip c4 launch the sweep times (unit counts, clip offsets and 32-bit index math at
+    full size): clips 0, 131 and 255 of the one launch against the oracle."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    x = np.empty((256, 160000), np.float32)
+    with ThreadPoolExecutor(16) as ex:
+        list(ex.map(lambda c: x.__setitem__(c, synth.make_clip(4, c)), range(256)))
+    sc = synth.config_scales(4)
+    plan = wh.CwthPlan(sc, None, hop, 160000, wavelet="rmor", output="abs", max_clips=256, engine="umma")
+    out = plan.execute(torch.from_numpy(x).cuda())
+    ids = [0, 131, 255]
+    got = out[ids].cpu().numpy()
+    plan.close()
+    ref = O.cwth_batch(x[ids], sc, hop, wavelet="rmor", output="abs", threads=16)
+    assert row_rel_err(got, ref) <= ROW_TOL
+
+
 def test_c4_hop_columns_are_full_transform_columns():
     """test_wavelet.py:245-252 at BASELINE size: cwth(hop)[:, k] == cwth(1)[:, k*hop]."""
     x = synth.make_batch(4, clips=1, start=3)
