@@ -43,7 +43,7 @@
 namespace wh {
 
 // converter warps: 6 (16 warps in all: 4 per SM sub-partition, so 128 registers per thread)
-// -- the window conversion is issue-bound and 6 warps beat 4 (c2 68.5 -> 64.4 us, c4 hop 64
+// -- 6 warps keep more window loads in flight than 4 (c2 68.5 -> 64.4 us, c4 hop 64
 // 228 -> 208 us, hop 256 / 1024 225 -> 205 us, c5 -1 %; profiles/r02h_ab.txt); 8 warps would
 // cap registers at 96 and spill
 #ifndef WH_CONV_WARPS
@@ -710,7 +710,7 @@ __device__ __forceinline__ int window_exponent(float mx) {
 
 // Split two samples into hi / lo fp16 pairs: hi = rn16(x 2^e), lo = rn16(x 2^e - hi).  The
 // scale and the residual use the packed fp32x2 pipe (FMUL2 / FADD2): 6 instructions per pair
-// instead of 8 -- the window conversion is issue-bound.
+// instead of 8 (measured neutral: the conversion waits on its loads, not on issue).
 __device__ __forceinline__ void split2(float x0, float x1, uint64_t sc2, uint32_t &hw, uint32_t &lw) {
     uint64_t a2, p;
     asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(x0), "f"(x1));
