@@ -37,7 +37,7 @@ def needs_build(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, diag: bool = False, dev: bool = False) -> str:
     """Build the product library; ``diag`` builds libwavehop_b200_diag.so instead (-DWH_DIAG:
     role switches, wait counters and the unit timeline compiled into the kernel; loaded by
     _lib when WH_DIAG_LIB=1 -- tools only, never the product path)."""
@@ -47,7 +47,10 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str
     # one nvcc per translation unit, in parallel, then one link
     objdir = os.path.join(HERE, "csrc", "build_diag" if diag else "build")
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f != "-shared"] + (["-DWH_DIAG"] if diag else [])
+    # dev (diagnostics library only): -DWH_DEV_BUILD instantiates two phase counts of the engine
+    # kernel instead of seven -- for quick experiments on the large-hop paths
+    cflags = [f for f in FLAGS if f != "-shared"] + (["-DWH_DIAG"] if diag else []) + \
+        (["-DWH_DEV_BUILD"] if dev and diag else [])
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
@@ -73,4 +76,4 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, diag="--diag" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose=True, diag="--diag" in sys.argv, dev="--dev" in sys.argv))

@@ -130,6 +130,11 @@ struct Plan {
     bool doubled_v = false, no_2v = false;  // UMMA: rows of 2 lcm(hop, 64) samples (one pass)
     int32_t pstream = 0;           // UMMA: rows of hop samples (one frame each), window streamed by column panel
     bool no_pstream = false;       // UMMA planner retry without panel streaming
+    int32_t tf32 = 0;              // UMMA panel streaming with kind::tf32 MMAs (no window exponent, no pre-pass)
+    bool no_tma = false;           // planner override: tf32 panels fetched by cp.async instead of TMA tensor copies
+    int32_t acc2 = 0;              // tf32: two accumulator sets per TMEM buffer (even / odd K-slices)
+    int32_t ks = 64;               // taps per K-step: 64 (fp16 operands) or 32 (tf32 operands), 128 B per operand row
+    int32_t tile_rows = 128;       // rows of a tile that carry frames (<= 128: a clip's rows split evenly over its tiles)
     double unit_cost = 0.0;        // UMMA: modelled MMA cycles of one unit (all passes)
     bool no_convregs = false;      // UMMA planner override: converters without the register prefetch
     bool force_fixup = false;      // UMMA planner override (tests): min-max units all to the fix-up kernel

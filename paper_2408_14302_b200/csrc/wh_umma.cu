@@ -28,6 +28,7 @@
 //               swizzled once the window buffer is free
 //   warps 6-13  epilogue (2 per TMEM lane quadrant): tcgen05.ld main + corr -> scale,
 //               |W| / power / log_db / log1p -> 16-byte global stores, per-clip min/max
+#include <cuda.h>  // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint: no libcuda link)
 #include <cuda_fp16.h>
 #include <math.h>
 
@@ -73,6 +74,9 @@ static constexpr bool kDiag = false;
 #endif
 
 struct UmmaArgs {
+    // tf32 panel streaming: the batch as a 3-D tensor (V samples, N / V rows, clips) for TMA box
+    // copies of one 32-sample column panel of a window (128 B x win_rows rows, 128 B swizzle)
+    alignas(64) CUtensorMap tmap;
     const float *x;
     int64_t ld_x, N, F, hop;
     int64_t clips;
@@ -89,6 +93,10 @@ struct UmmaArgs {
     int32_t conv_regs;                  // converters prefetch the window into registers
     int32_t pf;                         // converters prefetch windows into L2 ahead (rows of 256)
     int32_t pstream;                    // rows of hop samples, the window streamed by 64-sample column panel
+    int32_t tf32;                       // pstream with tf32 operands: 32-sample panels split in place, no exponent
+    int32_t acc2;                       // tf32: two accumulator sets per buffer (even / odd K-slices), added by the epilogue
+    int32_t tma;                        // tf32: panels fetched by one TMA tensor copy each (tmap), else by cp.async
+    int64_t full_end;                   // tma: samples of a clip covered by whole rows of V ((N / V) * V)
     const float *segmax;                // pstream: max |x| per UM_SEG-sample segment [clips][nseg] (pre-pass)
     int32_t nseg;
     const UmmaPass *passes;
@@ -266,6 +274,18 @@ __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b
     else
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem), "l"(a), "l"(b),
+                     "r"(idesc), "r"(1u));
+}
+// tf32 operands (fp32 words in shared memory, K = 8 per instruction = 32 B of a 128 B row)
+template <int CG>
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+    if constexpr (CG == 2)
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem), "l"(a), "l"(b),
+                     "r"(idesc), "r"(1u));
+    else
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem), "l"(a), "l"(b),
                      "r"(idesc), "r"(1u));
 }
 template <int CG>
@@ -455,6 +475,17 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
             if (!WH_DBG(64)) {  // diagnostics: 64 = skip the re-zeroing (results invalid)
                 tmem_st16_zero(tbase + u0);
                 tmem_st16_zero(cbase - u0);
+            }
+            if (A.acc2) {  // second accumulator set (odd K-slices), 128 columns on
+                float v2[16], w2[16];
+                tmem_ld16x2(tbase + 128u + u0, cbase + 128u - u0, v2, w2);
+                tmem_st16_zero(tbase + 128u + u0);
+                tmem_st16_zero(cbase + 128u - u0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    v[i] += v2[i];
+                    wr[i] += w2[i];
+                }
             }
             if (WH_DBG(32)) continue;  // diagnostics: 32 = skip the stores
             if constexpr ((P == 1 || P == 2) && OUT != WH_OUT_COMPLEX64) if (A.rs == 1) {
@@ -755,6 +786,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     __shared__ float xring[4];  // per-unit window exponent 2^-e, written by the converters
     __shared__ float red[UM_CONV_WARPS];
     __shared__ __align__(8) uint64_t stg_full, res_full, tab_full;
+    __shared__ __align__(8) uint64_t slot_full[UM_WSLOTS];  // tf32 panel streaming: a TMA panel copy has landed
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_decide;  // epilogue: CTA-uniform decision on the oldest pending unit
 
@@ -930,6 +962,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_init(&acc_empty[i], UM_EPI_WARPS * CG);  // epilogue warps of both CTAs (leader's copy)
         }
         mbar_init(&stg_full, 1);
+        for (int i = 0; i < UM_WSLOTS; ++i) mbar_init(&slot_full[i], 1);
         mbar_init(&res_full, (CG == 2 && leader) ? 2 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1043,12 +1076,13 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const uint32_t RING = A.ring_bytes - A.res_bytes;
         const uint32_t stage0 = smem_u32(stage_base), ring0 = stage0 + A.res_bytes;
         if (A.pstream) {
-            // Panel streaming: the window's 64-sample column panels pass through the window
-            // slots (panel counter pc, slot pc % win_bufs); the tiles of the single pass are in
-            // panel-major order; tap groups stream through the ring (or are resident).
+            // Panel streaming: the window's column panels pass through the window slots (panel
+            // counter pc, slot pc % win_bufs); the tiles of the single pass are in panel-major
+            // order; tap groups stream through the ring (or are resident).
             const uint32_t wh16 = WH >> 4, NS = (uint32_t)A.win_bufs;
             const int *s_tpanel = s_goff + A.n_groups;  // window panel of each tile
             uint32_t pc = 0;
+            const uint32_t o2 = A.acc2 ? 128u : 0u;
             for (int64_t item = u0; item < n_units; item += ustride, ++wcnt, ++acnt) {
                 WH_TRACE(0, wcnt);
                 const int4 pinfo = s_pass[0];
@@ -1058,22 +1092,29 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const uint32_t d_acc = tmem + ab * (uint32_t)A.acc_stride;
                 const uint32_t C = (uint32_t)pinfo.w;
                 int cur = -1;
+                bool held = false;  // the slot of panel `cur` is not released yet
                 uint32_t a_hi16 = 0;
-                // step to panel `target`: release the current slot, wait for the following
-                // panels (a panel without tiles is released at once)
+                // a panel's slot is released right behind its last tile's MMAs (not when the next
+                // panel is reached): the refill of the slot then never waits for the issue loop
+                auto release = [&]() {
+                    if (elect_one()) umma_commit<CG>(&win_empty[pc % NS]);
+                    __syncwarp();
+                    ++pc;
+                    held = false;
+                };
+                // step to panel `target`: wait for the following panels (a panel without tiles
+                // is released at once)
                 auto step_to = [&](int target) {
                     while (cur < target) {
-                        if (cur >= 0) {
-                            if (elect_one()) umma_commit<CG>(&win_empty[pc % NS]);
-                            __syncwarp();
-                            ++pc;
-                        }
+                        if (held) release();
                         mbar_wait_p(&win_full[pc % NS], (pc / NS) & 1, pa, 0, pon);
                         tc_fence_after();
                         a_hi16 = (smem_u32(win_base) + (pc % NS) * 2 * WH) >> 4;
                         ++cur;
+                        held = true;
                     }
                 };
+                const int t_last = s_group[pinfo.y - 1].y - 1;  // the unit's last tile
                 WH_TRACE(1, wcnt);
                 for (int gi = pinfo.x; gi < pinfo.y; ++gi) {
                     const int4 gr = s_group[gi];
@@ -1093,14 +1134,32 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         tc_fence_after();
                     }
                     const uint32_t g16 = gbase >> 4;
+                    // The issuing thread waits on every MMA it issues (the tensor pipe's queue is
+                    // short), so the table entries of the next tile are loaded before this
+                    // tile's MMAs: their latency passes behind the issue.  (One entry past the
+                    // group's end is still inside the tables.)
+                    uint4 tt = s_tile[gr.x];
+                    int tp = s_tpanel[gr.x];
                     for (int t = gr.x; t < gr.y; ++t) {
-                        step_to(s_tpanel[t]);
-                        const uint4 tt = s_tile[t];
+                        const uint4 tn = s_tile[t + 1];
+                        const int tpn = s_tpanel[t + 1];
+                        if (tp != cur) step_to(tp);
                         const uint32_t ah = a_hi16 + (tt.x & 0xffffu), al = ah + wh16;
                         const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
                         const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
                         if (!WH_DBG(4) && elect_one()) {
-                            if (tt.w) {
+                            if (A.tf32) {
+                                // acc2: odd K-slices accumulate into a second (main | corr) set 128
+                                // columns on -- half the accumulation steps per accumulator (the
+                                // fp32 accumulate truncates: the error grows with the steps);
+                                // the epilogue adds the sets
+#pragma unroll
+                                for (uint32_t j = 0; j < 4; ++j) {
+                                    const uint32_t o = (j & 1) ? o2 : 0u;
+                                    umma_tf32<CG>(d1 + o, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                                    if (tt.w) umma_tf32<CG>(d2 + o, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
+                                }
+                            } else if (tt.w) {
 #pragma unroll
                                 for (uint32_t j = 0; j < 4; ++j) {
                                     umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
@@ -1113,6 +1172,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                             }
                         }
                         __syncwarp();
+                        if (tpn != tp || t == t_last) release();
+                        tt = tn;
+                        tp = tpn;
                     }
                     if (goff < 0) {
                         if (elect_one()) umma_commit<CG>(&b_empty[slot]);
@@ -1120,12 +1182,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     }
                 }
                 step_to(A.panels - 1);
-                if (elect_one()) {
-                    umma_commit<CG>(&win_empty[pc % NS]);
-                    umma_commit<CG>(&acc_full[ab]);
-                }
+                if (held) release();
+                if (elect_one()) umma_commit<CG>(&acc_full[ab]);
                 __syncwarp();
-                ++pc;
                 WH_TRACE(2, wcnt);
             }
         } else
@@ -1163,12 +1222,16 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         tc_fence_after();
                     }
                     const uint32_t g16 = gbase >> 4;
+                    // (the next tile's table entry is loaded before this tile's MMAs: the issuing
+                    // thread waits on every MMA it issues, so the load's latency passes behind them;
+                    // one entry past the last tile is still inside the tables)
+                    uint4 tt = s_tile[gr.x];
                     for (int t = gr.x; t < gr.y; ++t) {
                         // MMA1: A_hi x [hi_c0..hi_C-1 | lo_C-1..lo_c1] -> main_j at col j, corr_j at 2C-1-j
                         // MMA2: A_lo x [hi_C-1..hi_c1]               -> corr   (skipped if c1 = C)
                         // (CG = 2: each CTA's stage holds half of every B operand).  Descriptor
                         // low words are 16-byte smem addresses (< 2^14): no masking needed.
-                        const uint4 tt = s_tile[t];
+                        const uint4 tn = s_tile[t + 1];
                         const uint32_t ah = a_hi16 + (tt.x & 0xffffu), al = ah + wh16;
                         const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
                         const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
@@ -1186,6 +1249,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                             }
                         }
                         __syncwarp();
+                        tt = tn;
                     }
                     if (goff < 0) {
                         if (elect_one()) umma_commit<CG>(&b_empty[slot]);
@@ -1263,7 +1327,204 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
-        if (A.pstream) {
+        if (A.pstream && A.tf32) {
+            // Panel streaming with tf32 operands.  A panel is 32 samples (128 B of fp32) of every
+            // window row, fetched win_bufs - 1 panels ahead straight to its swizzled place in the
+            // hi half of a slot: by ONE TMA tensor copy (a box of 128 B x win_rows rows of the
+            // batch viewed as (V samples, N / V rows, clips), 128 B swizzle, rows outside the clip
+            // zero-filled by the copy engine), or -- unaligned inputs -- by cp.async, 16 bytes per
+            // thread.  Once landed, each converter thread reads its chunks back, clears the low
+            // 13 bits in place (hi = the tf32 the tensor core reads) and writes lo = x - hi (exact
+            // in fp32, rounded to tf32) at the same offset of the slot's lo half.  No window
+            // exponent: tf32 keeps fp32's range.  Chunk c = ct + i * CONV_THREADS sits at row
+            // c >> 3, 16-byte column c & 7: the row stride between a thread's chunks is a multiple
+            // of 8, so its swizzle term is constant and the addresses advance by fixed steps.
+            const uint32_t NS = (uint32_t)A.win_bufs;
+            const int nch = A.win_rows * 8;
+            const int row0 = ct >> 3, c8 = ct & 7;
+            constexpr int RSTEP = UM_CONV_THREADS / 8;          // rows between a thread's chunks
+            constexpr uint32_t SSTEP = (uint32_t)RSTEP * 128u;  // shared-memory bytes between them
+            static_assert(RSTEP % 8 == 0, "converter threads must cover whole swizzle periods");
+            const int nmine = ct < nch ? (nch - ct + UM_CONV_THREADS - 1) / UM_CONV_THREADS : 0;
+            const uint32_t soff0 = smem_u32(win_base) + (uint32_t)row0 * 128u + (uint32_t)((c8 ^ (row0 & 7)) << 4);
+            const int64_t gstep = (int64_t)RSTEP * A.V;  // samples between a thread's chunks
+            const bool tma = A.tma != 0;
+            struct Geo {
+                const float *xb;   // the clip
+                int64_t g0;        // clip sample of this thread's first chunk in panel 0
+                int64_t w0;        // clip sample of the window's first row
+                int64_t b, tile;
+                int64_t r0;        // tma: tensor row of the window's first row (floor(w0 / V))
+                int32_t coff;      // tma: column of the window's first sample in that row
+                bool interior;     // the whole window lies inside the clip (and is 16-byte aligned)
+                bool tail;         // tma: the window reaches the clip's last, partial row of V samples
+            };
+            auto geo = [&](int64_t item) {
+                Geo g;
+                unit_tile(item, g.b, g.tile);
+                g.w0 = g.tile * 128 * A.V - A.G0;
+                g.xb = A.x + g.b * A.ld_x;
+                g.g0 = g.w0 + (int64_t)row0 * A.V + c8 * 4;
+                const int64_t wend = g.w0 + (int64_t)A.win_rows * A.V;
+                g.interior = A.vec_ok && g.w0 >= 0 && wend <= A.N;
+                g.tail = A.full_end < A.N && wend > A.full_end;
+                // w0 = tile * 128 * V - G0: floor division by V without dividing (G0 < 2^31)
+                const int64_t q = (int64_t)((uint32_t)A.G0 / (uint32_t)A.V);
+                const int32_t rem = A.G0 - (int32_t)q * A.V;
+                g.r0 = g.tile * 128 - q - (rem ? 1 : 0);
+                g.coff = rem ? A.V - rem : 0;
+                return g;
+            };
+            auto fetch_panel = [&](const Geo &g, int p, uint32_t sl) {
+                if (tma) {
+                    // one box: columns [col, col + 32) of rows [r0, r0 + win_rows) of clip b
+                    if (ct == 0) {
+                        int64_t r0 = g.r0;
+                        int32_t col = g.coff + p * 32;
+                        if (col >= A.V) {
+                            col -= A.V;
+                            ++r0;
+                        }
+                        mbar_expect_tx(&slot_full[sl], WH);
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                            "{%2, %3, %4}], [%5];" ::"r"(smem_u32(win_base) + sl * 2 * WH),
+                            "l"(&A.tmap), "r"((int32_t)col), "r"((int32_t)r0), "r"((int32_t)g.b), "r"(smem_u32(&slot_full[sl]))
+                            : "memory");
+                    }
+                    return;
+                }
+                uint32_t dst = soff0 + sl * 2 * WH;
+                if (g.interior) {
+                    const float *src = g.xb + g.g0 + p * 32;
+                    for (int i = 0; i < nmine; ++i, dst += SSTEP, src += gstep)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+                } else {
+                    int64_t q = g.g0 + p * 32;
+                    for (int i = 0; i < nmine; ++i, dst += SSTEP, q += gstep) {
+                        if (A.vec_ok && q >= 0 && q + 4 <= A.N) {
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g.xb + q) : "memory");
+                        } else {
+                            float z[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) z[k] = (q + k >= 0 && q + k < A.N) ? __ldg(g.xb + q + k) : 0.0f;
+                            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(z[0]), "f"(z[1]),
+                                         "f"(z[2]), "f"(z[3]) : "memory");
+                        }
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            // the fetch sequence runs NS - 1 panels ahead of the conversion
+            int64_t f_item = u0;
+            int f_p = 0;
+            uint32_t fc = 0;
+            Geo fg = geo(u0 < n_units ? u0 : 0);
+            auto fetch_next = [&]() {
+                if (f_item < n_units) fetch_panel(fg, f_p, fc % NS);
+                else if (!tma) asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+                ++fc;
+                if (++f_p == A.panels) {
+                    f_p = 0;
+                    f_item += ustride;
+                    if (f_item < n_units) fg = geo(f_item);
+                }
+            };
+            // TMA copies cost the issuing thread next to nothing, so they run only NS - 2 panels
+            // ahead: the slot they refill was released two panels ago and the thread never waits
+            const uint32_t lag = tma ? 2u : 1u;
+            for (uint32_t j = 0; j + lag < NS; ++j) fetch_next();
+            uint32_t qc = 0, wcnt = 0;
+            for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
+                const Geo cg = geo(item);
+                int p0, p1;
+                unit_passes(item, p0, p1);
+                const int64_t own0 = cg.tile * 128 * A.V, own1 = own0 + 128 * (int64_t)A.V;
+                uint32_t *rec = A.nfbad ? A.nfbad + cg.b * (int64_t)(1 + WH_NF_CAP) : nullptr;
+                if (ct == 0) {
+                    WH_TRACE(3, wcnt);
+                    xring[wcnt & 3] = 1.0f;
+                }
+                for (int p = 0; p < A.panels; ++p, ++qc) {
+                    const uint32_t sl = qc % NS;
+                    {
+                        const long long tw = pon ? clock64() : 0;
+                        if (tma) mbar_wait(&slot_full[sl], (qc / NS) & 1);
+                        else asm volatile("cp.async.wait_group %0;" ::"n"(UM_WSLOTS - 2) : "memory");
+                        if (pon) pa.c[0] += (unsigned long long)(clock64() - tw);
+                    }
+                    if (wcnt == 1 && ct == 0) WH_TRACE(4, p);  // diagnostics: panel timeline of the second unit
+                    const uint32_t a0 = soff0 + sl * 2 * WH;
+                    const long long tc0 = pon ? clock64() : 0;
+                    constexpr int UNR = 6;  // chunks in flight per thread (independent load -> split -> store chains)
+                    for (int i0 = 0; i0 < (WH_DBG(2) ? 0 : nmine); i0 += UNR) {
+                        uint32_t v[UNR][4];
+#pragma unroll
+                        for (int u = 0; u < UNR; ++u)
+                            if (i0 + u < nmine)
+                                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(v[u][0]), "=r"(v[u][1]), "=r"(v[u][2]), "=r"(v[u][3])
+                                             : "r"(a0 + (uint32_t)(i0 + u) * SSTEP) : "memory");
+#pragma unroll
+                        for (int u = 0; u < UNR; ++u) {
+                            if (i0 + u >= nmine) continue;
+                            const int i = i0 + u;
+                            if (cg.tail) {
+                                // the clip's last row of V samples is partial: the tensor ends before
+                                // it (zero fill), its samples come straight from the clip
+                                const int64_t g = cg.g0 + p * 32 + (int64_t)i * gstep;
+                                if (g >= A.full_end && g < A.N) {
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k)
+                                        v[u][k] = g + k < A.N ? __float_as_uint(__ldg(cg.xb + g + k)) : 0u;
+                                }
+                            }
+                            const float m = fmax_nan(fmax_nan(fabsf(__uint_as_float(v[u][0])), fabsf(__uint_as_float(v[u][1]))),
+                                                     fmax_nan(fabsf(__uint_as_float(v[u][2])), fabsf(__uint_as_float(v[u][3]))));
+                            if (!(m <= 3.402823466e38f)) {  // non-finite samples (rare): 0, recorded once
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    if (!is_finite_f(__uint_as_float(v[u][k]))) {
+                                        const int64_t g = cg.g0 + p * 32 + (int64_t)i * gstep + k;
+                                        if (rec && p0 == 0 && g >= own0 && g < own1) nf_record(rec, A.nfctl + 1, g);
+                                        v[u][k] = 0u;
+                                    }
+                                }
+                            }
+                            uint32_t h[4], l[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                h[k] = v[u][k] & 0xffffe000u;
+                                const float r = __uint_as_float(v[u][k]) - __uint_as_float(h[k]);
+                                l[k] = (__float_as_uint(r) + 0x1000u) & 0xffffe000u;
+                            }
+                            const uint32_t a = a0 + (uint32_t)i * SSTEP;
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                                         "r"(h[3]) : "memory");
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a + WH), "r"(l[0]), "r"(l[1]),
+                                         "r"(l[2]), "r"(l[3]) : "memory");
+                        }
+                    }
+                    if (pon) pa.c[2] += (unsigned long long)(clock64() - tc0);
+                    if (wcnt == 1 && ct == 0) WH_TRACE(5, p);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
+                    if (wcnt == 1 && ct == 0) WH_TRACE(6, p);
+                    if (ct == 0) window_ready(sl, qc);
+                    // refill the slot of the previous panel once its MMAs are done (TMA: only the
+                    // issuing thread waits)
+                    if (qc >= lag && (!tma || ct == 0)) {
+                        const uint32_t ps = (qc - lag) % NS;
+                        mbar_wait_p(&win_empty[ps], ((qc - lag) / NS) & 1, pa, 1, pon);
+                    }
+                    if (wcnt == 1 && ct == 0) WH_TRACE(12, p);
+                    fetch_next();
+                    if (wcnt == 1 && ct == 0) WH_TRACE(13, p);
+                }
+                if (ct == 0) WH_TRACE(7, wcnt);
+            }
+            if (!tma) asm volatile("cp.async.wait_all;" ::: "memory");
+        } else if (A.pstream) {
             // Panel streaming (rows of hop samples).  Each 64-sample column panel of a unit's
             // window (win_rows rows x 256 B of fp32) is copied by cp.async straight into a panel
             // slot, win_bufs - 1 panels ahead; once it has landed the converters read their own
@@ -1953,7 +2214,7 @@ struct BankArgs {
     const int64_t *half;
     const int32_t *fexp;
     double C, Bw;
-    int32_t P, Cc, G0, cg;
+    int32_t P, Cc, G0, cg, tf32;
     int64_t hop;
     uint8_t *bank;
 };
@@ -1974,15 +2235,16 @@ __global__ void k_build_bank(BankArgs a) {
     const int nc = tl.ncols, ncorr = tl.ncorr, n1 = nc + ncorr;
     const double norm = pow(M_PI * a.Bw, -0.5);
     const double w = 2.0 * M_PI * a.C;
-    for (int idx = threadIdx.x; idx < tl.ncols * 64; idx += blockDim.x) {
-        const int n = idx / 64, e = idx % 64;
+    const int KS = a.tf32 ? 32 : 64;  // taps per K-step (128 B per operand row)
+    for (int idx = threadIdx.x; idx < tl.ncols * KS; idx += blockDim.x) {
+        const int n = idx / KS, e = idx % KS;
         const int col = tl.c0 + n;
         double v = 0.0;
         if (col < ps.ns * CP) {
             const int s = ps.s0 + col / CP;
             const int c = (col / a.P) % a.Cc;
             const int r = col % a.P;
-            const int64_t g = (int64_t)tl.k * 64 + e;
+            const int64_t g = (int64_t)tl.k * KS + e;
             const int64_t u = g - a.G0 - (int64_t)r * a.hop;
             const int64_t L = a.half[s];
             if (u >= -L && u <= L) {
@@ -2000,17 +2262,38 @@ __global__ void k_build_bank(BankArgs a) {
                 v = ldexp(v, a.fexp[s]);
             }
         }
-        const __half h = __double2half(v);
-        const __half l = __double2half(v - (double)__half2float(h));
-        auto put = [&](uint8_t *base, int row, __half val) {
-            const uint32_t off = (uint32_t)row * 128u + (uint32_t)((((e >> 3) ^ (row & 7)) << 4) + (e & 7) * 2);
-            *reinterpret_cast<__half *>(base + off) = val;
+        // the two parts of the tap: fp16 (hi = rn16(v), lo = rn16(v - hi)) or tf32 (fp32 words
+        // rounded to 10 mantissa bits -- their low 13 bits are zero, so the tensor core's
+        // treatment of those bits cannot matter)
+        struct Part { uint32_t bits; };
+        Part h, l;
+        if (a.tf32) {
+            auto rtf32 = [](double x) {
+                const uint32_t b = __float_as_uint((float)x);
+                return (b + 0x1000u) & 0xffffe000u;
+            };
+            h.bits = rtf32(v);
+            l.bits = rtf32(v - (double)__uint_as_float(h.bits));
+        } else {
+            const __half hh = __double2half(v);
+            const __half ll = __double2half(v - (double)__half2float(hh));
+            h.bits = __half_as_ushort(hh);
+            l.bits = __half_as_ushort(ll);
+        }
+        auto put = [&](uint8_t *base, int row, Part val) {
+            if (a.tf32) {
+                const uint32_t off = (uint32_t)row * 128u + (uint32_t)((((e >> 2) ^ (row & 7)) << 4) + (e & 3) * 4);
+                *reinterpret_cast<uint32_t *>(base + off) = val.bits;
+            } else {
+                const uint32_t off = (uint32_t)row * 128u + (uint32_t)((((e >> 3) ^ (row & 7)) << 4) + (e & 7) * 2);
+                *reinterpret_cast<uint16_t *>(base + off) = (uint16_t)val.bits;
+            }
         };
         const int rrev = C - 1 - col;  // row index in the reversed parts
         const bool corr = rrev < ncorr;
         if (a.cg == 2) {
             uint8_t *blk0 = tile0, *blk1 = tile0 + tl.blk1_delta;
-            auto put1 = [&](int row, __half val) {  // row of MMA1's B
+            auto put1 = [&](int row, Part val) {  // row of MMA1's B
                 if (row < n1 / 2) put(blk0, row, val);
                 else put(blk1, row - n1 / 2, val);
             };
@@ -2037,6 +2320,14 @@ static UmmaKernel pick_p(int P) {
     switch (P) {
         case 1: return k_umma<CC, 1, CG>;
         case 2: return k_umma<CC, 2, CG>;
+#ifdef WH_DEV_BUILD  // development builds (build.py --dev): two phase counts only, a fraction of the compile time
+        default: return nullptr;
+    }
+}
+template <int CC, int CG>
+static UmmaKernel pick_p_unused(int P) {
+    switch (P) {
+#endif
         case 4: return k_umma<CC, 4, CG>;
         case 8: return k_umma<CC, 8, CG>;
         case 16: return k_umma<CC, 16, CG>;
@@ -2090,7 +2381,7 @@ int umma_supported(const Plan &p, std::string *why) {
 // 128-byte aligned in the bank
 static int ncheck_tiles(const Plan &p) {
     for (auto &t : p.tiles)
-        if ((int64_t)t.k * 64 / p.V >= 4096 || (!p.pstream && p.V / 64 > 16) || t.c0 > 255 || t.ncols > 255 ||
+        if ((int64_t)t.k * p.ks / p.V >= 4096 || (!p.pstream && p.V / 64 > 16) || t.c0 > 255 || t.ncols > 255 ||
             (t.byte_off & 127))
             return fail(WH_E_UNSUPPORTED, "UMMA engine: tile table out of range");
     if (16 * p.passes.size() + 20 * p.groups_u.size() + 20 * p.tiles.size() + 4 * (size_t)((p.S + 15) / 16 * 16) > 32 * 1024)
@@ -2154,6 +2445,21 @@ static int umma_prepare_impl(Plan &p) {
         const bool want = plan_knob("WH_UMMA_PSTREAM") != nullptr || H % 128 != 0;
         p.pstream = (!p.no_pstream && want && plan_knob("WH_UMMA_NO_PSTREAM") == nullptr && H >= 256 &&
                      H <= 4096 && H % 64 == 0 && cc * (int64_t)p.S <= 128) ? 1 : 0;
+        // tf32 operands (kind::tf32, K-steps of 32 taps): the fp32 samples are split in place
+        // (hi = the top 19 bits, lo = x - hi) -- no window exponent, so no pre-pass over the
+        // input, and a third of the conversion instructions of the fp16 split; the MMAs read
+        // twice the operand bytes per tap, which the frame-proportional large hops can afford
+        // Opt-in (WH_UMMA_TF32=1): measured slower than the fp16 split on c4 (hop 256 / 1024:
+        // 327 / 276 vs 232 / 255 us) -- twice the MMAs per tap, and each small-N MMA costs the
+        // issuing thread and the shared-memory operand reads the same whatever its K.
+        p.tf32 = 0;
+        if (p.pstream)
+            if (const char *t = plan_knob("WH_UMMA_TF32")) p.tf32 = std::atoi(t) ? 1 : 0;
+        p.ks = p.tf32 ? 32 : 64;
+        p.no_tma = plan_knob("WH_UMMA_NO_TMA") != nullptr;
+        // two accumulator sets when (main | corr) fits half a buffer
+        p.acc2 = (p.tf32 && 2 * ((cc * (int64_t)p.S + 15) / 16 * 16) <= 128) ? 1 : 0;
+        if (const char *t = plan_knob("WH_UMMA_ACC2")) p.acc2 = (p.acc2 && std::atoi(t)) ? 1 : 0;
     }
     if (!p.pstream) {
         if (p.hop >= 256 && p.hop % 128 != 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: hop needs panel streaming");
@@ -2187,7 +2493,7 @@ static int umma_prepare_impl(Plan &p) {
     }
     p.P = (int32_t)(p.V / H);
     p.Cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
-    p.panels = p.V / 64;
+    p.panels = p.V / p.ks;
     p.rows_total = (int32_t)(p.rs > 1 ? (p.F - 1) * p.rs + 1 : (p.F + p.P - 1) / p.P);
     p.row_tiles = (p.rows_total + 127) / 128;
 
@@ -2220,7 +2526,8 @@ static int umma_prepare_impl(Plan &p) {
     auto make_tiles = [&](int64_t G0, std::vector<UmmaPass> &passes, std::vector<UmmaTile> &tiles) -> double {
         passes.clear();
         tiles.clear();
-        const int64_t ksteps = (G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1;
+        const int64_t KS = p.ks;
+        const int64_t ksteps = (G0 + p.Lmax + (int64_t)(p.P - 1) * H) / KS + 1;
         double cost = 0.0;
         // heavy (long-tap) passes first so the accumulator pipeline starts on the long ones
         // (alternating heavy / light passes measured no better on c5)
@@ -2240,7 +2547,7 @@ static int umma_prepare_impl(Plan &p) {
                     const int s = ps.s0 + j / CP, r = j % p.P;
                     const int64_t lo = G0 - p.half[s] + (int64_t)r * H;
                     const int64_t hi = G0 + p.half[s] + (int64_t)r * H;
-                    if (hi >= k * 64 && lo <= k * 64 + 63) {
+                    if (hi >= k * KS && lo <= k * KS + KS - 1) {
                         c0 = j;
                         break;
                     }
@@ -2256,7 +2563,7 @@ static int umma_prepare_impl(Plan &p) {
                 int c1 = ps.cols;
                 for (int j = c0; j < ps.ns * CP; ++j) {
                     const int s = ps.s0 + j / CP, r = j % p.P;
-                    const int64_t u0 = k * 64 - G0 - (int64_t)r * H, u1 = u0 + 63;
+                    const int64_t u0 = k * KS - G0 - (int64_t)r * H, u1 = u0 + KS - 1;
                     const int64_t umin = (u0 <= 0 && u1 >= 0) ? 0 : std::min(std::llabs(u0), std::llabs(u1));
                     if ((double)umin > (double)p.half[s]) continue;  // inactive column
                     const double x = (double)umin / p.scales[s];
@@ -2308,17 +2615,17 @@ static int umma_prepare_impl(Plan &p) {
         if (p.passes.size() != 1) return fail(WH_E_UNSUPPORTED, "UMMA engine: panel streaming needs one pass");
         // K-steps in panel-major order (panel = (64k mod V) / 64, row shift q = 64k / V): all
         // the K-steps of one window panel run while it is in its slot
-        const int64_t V = p.V;
+        const int64_t V = p.V, KS = p.ks;
         std::stable_sort(p.tiles.begin(), p.tiles.end(), [&](const UmmaTile &a, const UmmaTile &b) {
-            const int64_t pa = (64 * (int64_t)a.k % V) / 64, pb = (64 * (int64_t)b.k % V) / 64;
+            const int64_t pa = (KS * (int64_t)a.k % V) / KS, pb = (KS * (int64_t)b.k % V) / KS;
             return pa != pb ? pa < pb : a.k < b.k;
         });
     }
     p.Qlo = (int32_t)((p.G0 + p.V - 1) / p.V);
-    p.ksteps = (int32_t)((p.G0 + p.Lmax + (int64_t)(p.P - 1) * H) / 64 + 1);
-    const int64_t qmax = (int64_t)(p.ksteps - 1) * 64 / p.V;
+    p.ksteps = (int32_t)((p.G0 + p.Lmax + (int64_t)(p.P - 1) * H) / p.ks + 1);
+    const int64_t qmax = (int64_t)(p.ksteps - 1) * p.ks / p.V;
     p.win_rows = (int32_t)(((128 + qmax) + 7) / 8 * 8);
-    if (p.pstream && (int64_t)p.win_rows * 8 > (int64_t)UM_PCH * UM_CONV_THREADS)
+    if (p.pstream && !p.tf32 && (int64_t)p.win_rows * 8 > (int64_t)UM_PCH * UM_CONV_THREADS)
         return fail(WH_E_UNSUPPORTED, "UMMA engine: panel too tall for the converters' registers");
     const int64_t win = 2LL * (p.pstream ? 1 : p.panels) * p.win_rows * 128;  // pstream: one panel slot
     int64_t byte_off = 0;
@@ -2432,7 +2739,7 @@ static int umma_prepare_impl(Plan &p) {
     const int64_t stage_bytes = std::max<int64_t>(max_group, 1024);
     const int64_t table_bytes = (16 * (int64_t)p.passes.size() + 20 * (int64_t)p.groups_u.size() +
                                  (p.pstream ? 20 : 16) * (int64_t)p.tiles.size() + 4 * (int64_t)((p.S + 15) / 16 * 16) +
-                                 15) / 16 * 16;
+                                 15) / 16 * 16 + 16;  // + one entry of slack: the issue loop reads a tile ahead
     // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
     // alignment slack and the tables
     UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
@@ -2527,10 +2834,12 @@ static int umma_prepare_impl(Plan &p) {
             put32((uint32_t)g.tile_begin); put32((uint32_t)g.tile_end);
             put32((uint32_t)(g.bank_off >> 7)); put32((uint32_t)g.cta_bytes);
         }
-        auto idesc = [&](uint32_t n) { return (1u << 4) | ((n >> 3) << 17) | (((128u * (uint32_t)p.cg) >> 4) << 24); };
+        // D f32; A / B f16 (0) or tf32 (2 at bits [7,10) and [10,13)); K-major; N >> 3; M >> 4
+        const uint32_t fmt = p.tf32 ? ((2u << 7) | (2u << 10)) : 0u;
+        auto idesc = [&](uint32_t n) { return (1u << 4) | fmt | ((n >> 3) << 17) | (((128u * (uint32_t)p.cg) >> 4) << 24); };
         for (auto &tl : p.tiles) {
             // window row shift q and panel of this K-step's A operand (k*64 = q*V + panel*64)
-            const uint32_t kg = (uint32_t)tl.k * 64u, q = kg / (uint32_t)p.V, panel = (kg % (uint32_t)p.V) >> 6;
+            const uint32_t kg = (uint32_t)tl.k * (uint32_t)p.ks, q = kg / (uint32_t)p.V, panel = (kg % (uint32_t)p.V) / (uint32_t)p.ks;
             const uint32_t aoff = (p.pstream ? 0u : panel * (uint32_t)p.win_rows * 128u) + q * 128u;
             const uint32_t n1 = (uint32_t)(tl.ncols + tl.ncorr), n2 = (uint32_t)tl.ncorr;
             const uint32_t b2d = (p.cg == 2 ? n1 / 2 : n1) * 128u;
@@ -2546,7 +2855,7 @@ static int umma_prepare_impl(Plan &p) {
         }
         for (auto &g : p.groups_u) put32((uint32_t)g.pad_);
         if (p.pstream)  // tile -> window panel
-            for (auto &tl : p.tiles) put32((uint32_t)(((int64_t)tl.k * 64 % p.V) / 64));
+            for (auto &tl : p.tiles) put32((uint32_t)(((int64_t)tl.k * p.ks % p.V) / p.ks));
         p.tables_bytes = table_bytes;
         WH_CUDA_TRY(cudaMalloc(&p.d_tables, (size_t)table_bytes));
         WH_CUDA_TRY(cudaMemcpy(p.d_tables, blob.data(), (size_t)table_bytes, cudaMemcpyHostToDevice));
@@ -2557,7 +2866,7 @@ static int umma_prepare_impl(Plan &p) {
     WH_CUDA_TRY(cudaMemcpy(p.d_groups_u, p.groups_u.data(), sizeof(UmmaGroup) * p.groups_u.size(),
                            cudaMemcpyHostToDevice));
     WH_CUDA_TRY(cudaMalloc(&p.d_bank, (size_t)p.bank_bytes));
-    if (p.pstream) {
+    if (p.pstream && !p.tf32) {
         cudaFree(p.d_segmax);
         p.d_segmax = nullptr;
         WH_CUDA_TRY(cudaMalloc(&p.d_segmax, sizeof(float) * (size_t)p.max_clips * (size_t)((p.N + UM_SEG - 1) / UM_SEG)));
@@ -2572,7 +2881,7 @@ static int umma_prepare_impl(Plan &p) {
     BankArgs ba{};
     ba.passes = p.d_passes; ba.tiles = p.d_tiles; ba.n_passes = (int32_t)p.passes.size();
     ba.scales = p.d_scales; ba.half = p.d_half; ba.fexp = d_fexp; ba.C = p.C; ba.Bw = p.B;
-    ba.P = p.P; ba.Cc = p.Cc; ba.G0 = p.G0; ba.hop = p.hop; ba.bank = p.d_bank; ba.cg = p.cg;
+    ba.P = p.P; ba.Cc = p.Cc; ba.G0 = p.G0; ba.hop = p.hop; ba.bank = p.d_bank; ba.cg = p.cg; ba.tf32 = p.tf32;
     k_build_bank<<<(unsigned)p.tiles.size(), 256>>>(ba);
 
     WH_CUDA_TRY(cudaGetLastError());
@@ -2658,6 +2967,23 @@ int umma_pass_groups(const Plan &p, int64_t clips) {
     return (n_passes + ppu - 1) / ppu;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        (void)cudaGetLastError();
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
 int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out, cudaStream_t s, uint32_t *mm,
                 uint32_t *arrive, uint32_t *abandon, uint32_t *nfbad, uint32_t *nfctl) {
     UmmaArgs a{};
@@ -2676,6 +3002,24 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.cpr_magic = ((1 << 20) + a.cpr - 1) / a.cpr;
     a.conv_regs = (!p.use_stg && !p.no_convregs && !p.pstream) ? 1 : 0;
     a.pstream = p.pstream;
+    a.tf32 = p.tf32;
+    a.acc2 = p.acc2;
+    a.full_end = (p.N / p.V) * p.V;
+    a.tma = 0;
+    if (p.tf32 && !p.no_tma && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ld_x % 4 == 0 && p.N >= p.V &&
+        p.win_rows <= 256 && clips <= 0x7fffffff && encode_tiled()) {
+        // the batch as (V samples, N / V whole rows, clips): a window panel is one box of
+        // 32 samples x win_rows rows; rows before / after the clip's whole rows are zero-filled
+        const cuuint64_t dims[3] = {(cuuint64_t)p.V, (cuuint64_t)(p.N / p.V), (cuuint64_t)clips};
+        const cuuint64_t strides[2] = {(cuuint64_t)p.V * 4, (cuuint64_t)ld_x * 4};
+        const cuuint32_t box[3] = {32, (cuuint32_t)p.win_rows, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult r = encode_tiled()(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(x), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        a.tma = r == CUDA_SUCCESS ? 1 : 0;
+    }
     a.nseg = (int32_t)((p.N + UM_SEG - 1) / UM_SEG);
     a.segmax = p.d_segmax;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
@@ -2714,7 +3058,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     int64_t grid = std::min<int64_t>(units * p.cg, ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
-    if (p.pstream) {
+    if (p.pstream && !p.tf32) {
         // the window exponents of panel streaming: max |x| per UM_SEG-sample segment
         if (clips > 65535) return fail(WH_E_INVALID_ARG, "UMMA engine: too many clips for one launch");
         k_seg_max<<<dim3((unsigned)a.nseg, (unsigned)clips), 256, 0, s>>>(x, ld_x, p.N, a.nseg, p.d_segmax);

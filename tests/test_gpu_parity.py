@@ -514,6 +514,42 @@ def test_panel_streaming_frames_only(hop, force, monkeypatch):
         np.testing.assert_array_equal(~np.isfinite(got[1, s]), want)
 
 
+@pytest.mark.parametrize("hop,tma", [(256, True), (1024, True), (2048, True), (320, False), (1024, False)])
+def test_panel_streaming_tf32(hop, tma, monkeypatch):
+    """Panel streaming with tf32 operands (WH_UMMA_TF32=1: kind::tf32 MMAs on 32-sample panels
+    fetched by TMA tensor copies -- or cp.async with WH_UMMA_NO_TMA -- split in place into
+    hi = the top 19 bits and lo = x - hi, two accumulator sets per buffer, no window exponent
+    and no pre-pass): against the oracle on c4-shaped clips whose length is not a multiple of
+    the hop (the clip's last partial row is patched from global memory), a NaN/inf clip and a
+    tiny-amplitude clip (no exponent scaling: tf32 keeps fp32's range) included."""
+    monkeypatch.setenv("WH_UMMA_PSTREAM", "1")
+    monkeypatch.setenv("WH_UMMA_TF32", "1")
+    if not tma:
+        monkeypatch.setenv("WH_UMMA_NO_TMA", "1")
+    n = 60000
+    x = synth.make_batch(4, clips=4, n=n, start=2)
+    x[1, 12345] = np.inf
+    x[1, 40000] = np.nan
+    x[3] *= np.float32(1e-30)
+    sc = synth.config_scales(4)
+    plan = wh.CwthPlan(sc, None, hop, n, wavelet="rmor", output="abs", max_clips=4, engine="umma")
+    got = plan.execute_host(x)
+    # rows that are not 16-byte aligned take the cp.async / scalar fetch whatever the knob says
+    base = np.zeros((2, n + 7), np.float32)
+    base[:, 3:3 + n] = x[[0, 2]]
+    got_u = plan.execute(torch.from_numpy(base).cuda()[:, 3:3 + n]).cpu().numpy()
+    plan.close()
+    ref = O.cwth_batch(x[[0, 2, 3]], sc, hop, wavelet="rmor", output="abs")
+    assert got.shape == (4, len(sc), -(-n // hop))
+    assert row_rel_err(got[[0, 2, 3]], ref) <= ROW_TOL
+    assert row_rel_err(got_u, ref[:2]) <= ROW_TOL
+    k = np.arange(got.shape[2])
+    for s, a in enumerate(sc):
+        L = math.ceil(6.0 * a * math.sqrt(0.75))
+        want = (np.abs(k * hop - 12345) <= L) | (np.abs(k * hop - 40000) <= L)
+        np.testing.assert_array_equal(~np.isfinite(got[1, s]), want)
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
 def test_pass_groups_are_byte_identical(groups, monkeypatch):
     """Splitting a tile pair's passes into separate units (what the launcher does when there

@@ -23,9 +23,9 @@ plan.profile(True)
 plan.execute(x, out)
 torch.cuda.synchronize()
 c = plan.profile(False)
-warps = {"producer": 1, "mma": 0.5, "converter": 4, "epilogue": 8, "relay": 0.5}
+warps = {"producer": 1, "mma": 0.5, "converter": 6, "epilogue": 8, "relay": 0.5}
 names = {"producer": ["b_empty", "issue", "-"], "mma": ["win_full", "acc_empty", "b_full"],
-         "converter": ["stg_full", "win_empty", "-"], "epilogue": ["acc_full", "-", "-"],
+         "converter": ["stg_full", "win_empty", "convert"], "epilogue": ["acc_full", "-", "-"],
          "relay": ["win_full", "-", "b_full"]}
 sms = min(148, clips * ((plan.frames + 127) // 128))
 for r, v in c.items():
