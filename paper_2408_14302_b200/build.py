@@ -47,10 +47,10 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False, dev: b
     # one nvcc per translation unit, in parallel, then one link
     objdir = os.path.join(HERE, "csrc", "build_diag" if diag else "build")
     os.makedirs(objdir, exist_ok=True)
-    # dev (diagnostics library only): -DWH_DEV_BUILD instantiates two phase counts of the engine
+    # dev (experiments only; never the shipped library): -DWH_DEV_BUILD instantiates two phase counts of the engine
     # kernel instead of seven -- for quick experiments on the large-hop paths
     cflags = [f for f in FLAGS if f != "-shared"] + (["-DWH_DIAG"] if diag else []) + \
-        (["-DWH_DEV_BUILD"] if dev and diag else [])
+        (["-DWH_DEV_BUILD"] if dev else [])
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")

@@ -239,8 +239,25 @@ __device__ __forceinline__ float apply_output(float mag, int output) {
         default: return mag;
     }
 }
+// |re + i im| without overflow / underflow of the squares (clips of any float32 amplitude: the
+// reference computes in float64): both parts are scaled by the power of two that brings the
+// larger one into [1, 2), and the root is scaled back -- the same bits as sqrt(re^2 + im^2)
+// wherever the squares are representable.
+__device__ __forceinline__ float cabs_scaled(float re, float im) {
+    const float m = fmaxf(fabsf(re), fabsf(im));
+    const uint32_t eb = __float_as_uint(m) & 0x7f800000u;         // exponent field of the larger part
+    if (eb == 0u || eb >= 0x7f000000u) {                           // zero / subnormal, or >= 2^127 (and inf / NaN)
+        if (!(m <= 3.402823466e38f)) return m != m ? m : INFINITY;  // NaN stays NaN, inf -> inf
+        const float s = eb == 0u ? 1.2676506e30f : 7.8886091e-31f;  // 2^100 / 2^-100
+        const float x = re * s, y = im * s;
+        return sqrtf(fmaf(x, x, y * y)) * (eb == 0u ? 7.8886091e-31f : 1.2676506e30f);
+    }
+    const float s = __uint_as_float(0x7f000000u - eb);              // 2^-e
+    const float x = re * s, y = im * s;
+    return sqrtf(fmaf(x, x, y * y)) * __uint_as_float(eb);
+}
 __device__ __forceinline__ float magnitude(float re, float im, int wavelet) {
-    return wavelet == WH_WAVELET_RMOR ? fabsf(re) : sqrtf(fmaf(re, re, im * im));
+    return wavelet == WH_WAVELET_RMOR ? fabsf(re) : cabs_scaled(re, im);
 }
 __device__ __forceinline__ bool is_finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
 // max that propagates NaN (and +inf through |x|): one test per window finds non-finite input

@@ -422,7 +422,7 @@ __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nval
         float val[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const float mag = (CC == 2) ? sqrtf(fmaf(re[r], re[r], im[r] * im[r])) : fabsf(re[r]);
+            const float mag = (CC == 2) ? cabs_scaled(re[r], im[r]) : fabsf(re[r]);
             val[r] = out_value<OUT>(mag);
         }
         if (A.minmax) {
@@ -457,7 +457,7 @@ __device__ __forceinline__ void store_run(const UmmaArgs &A, int64_t o, int nval
 // One accumulator buffer (a pass of ns scales) -> global, for this thread's row.  The two
 // epilogue warps of a TMEM lane quadrant split the 16-column units (half = 0 / 1); each
 // re-zeroes the main and correction columns it has read.
-template <int CC, int P, int OUT>
+template <int CC, int P, int OUT, int PS>
 __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, uint32_t tbase, uint32_t cbase,
                                          int s0, int ns, int cols, int half, int64_t b, int64_t frame0,
                                          int nvalid, float e, bool vec, float &lmin, float &lmax) {
@@ -476,7 +476,7 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                 tmem_st16_zero(tbase + u0);
                 tmem_st16_zero(cbase - u0);
             }
-            if (A.acc2) {  // second accumulator set (odd K-slices), 128 columns on
+            if (PS && A.acc2) {  // second accumulator set (odd K-slices), 128 columns on
                 float v2[16], w2[16];
                 tmem_ld16x2(tbase + 128u + u0, cbase + 128u - u0, v2, w2);
                 tmem_st16_zero(tbase + 128u + u0);
@@ -514,13 +514,17 @@ __device__ __forceinline__ void epi_pass(const UmmaArgs &A, const float *spow, u
                 for (int q = 0; q < SPU; ++q) {
 #pragma unroll
                     for (int r = 0; r < P; ++r) {
-                        const float x = (v[q * CP + r] + wr[15 - (q * CP + r)]) * f[q];
+                        // |W| from the accumulators' own scale (|acc| < 2^45: the squares neither
+                        // overflow nor underflow whatever the clip's amplitude), then the
+                        // power-of-two factor 2^-(e+f): the same bits as scaling re / im first
+                        // wherever those squares are representable
+                        const float xs = v[q * CP + r] + wr[15 - (q * CP + r)];
                         float mag;
                         if constexpr (CC == 2) {
-                            const float y = (v[q * CP + P + r] + wr[15 - (q * CP + P + r)]) * f[q];
-                            mag = sqrtf(fmaf(x, x, y * y));
+                            const float ys = v[q * CP + P + r] + wr[15 - (q * CP + P + r)];
+                            mag = sqrtf(fmaf(xs, xs, ys * ys)) * f[q];
                         } else {
-                            mag = fabsf(x);
+                            mag = fabsf(xs * f[q]);
                         }
                         val[q][r] = out_value<OUT>(mag);
                     }
@@ -774,7 +778,12 @@ __device__ __forceinline__ void chunk_rc(const UmmaArgs &A, int c, int &row, int
 }
 
 // ---- the kernel --------------------------------------------------------------------------
-template <int CC, int P, int CG>
+// Kernel variants (VS): 0 the common engine; 1 panel streaming (rows of hop samples, P = 1);
+// 2 the common engine with the per-clip arrival machinery of the opt-in min-max modes.  Each
+// variant's extra roles are compiled only there, so the common kernel keeps its size and
+// layout: with the panel-streaming converters inside it c2 ran 4 us slower (68.6 vs 64.4 us),
+// without them and the arrival code 2 us faster (62.5 us) -- instruction-cache footprint.
+template <int CC, int P, int CG, int VS>
 __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ UmmaArgs A) {
     extern __shared__ uint8_t smem_raw[];
     // 1 KB aligned (128 B swizzle atoms); pointer arithmetic on the shared array (not an
@@ -928,6 +937,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     };
     if (threadIdx.x == 64)
         for (int k = 1; k <= UM_PF; ++k) window_prefetch(u0 + k * ustride);
+    constexpr int PS = VS == 1 ? 1 : 0;  // panel streaming
     if (warp >= 2 && warp < 2 + UM_CONV_WARPS && A.conv_regs && u0 < n_units) conv_fetch(u0);
     const uint32_t WH = A.win_half_bytes;               // bytes of one (hi or lo) window
     uint8_t *win_base = smem;                            // [win_bufs][hi|lo][panels][rows][128]
@@ -1075,7 +1085,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         }
         const uint32_t RING = A.ring_bytes - A.res_bytes;
         const uint32_t stage0 = smem_u32(stage_base), ring0 = stage0 + A.res_bytes;
-        if (A.pstream) {
+        if (PS) {
             // Panel streaming: the window's column panels pass through the window slots (panel
             // counter pc, slot pc % win_bufs); the tiles of the single pass are in panel-major
             // order; tap groups stream through the ring (or are resident).
@@ -1327,7 +1337,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             mbar_expect_tx(&stg_full, bytes);
             if (bytes) bulk_g2s(stg + (lo - w0), A.x + b * A.ld_x + lo, bytes, &stg_full);
         };
-        if (A.pstream && A.tf32) {
+        if (PS && A.tf32) {
             // Panel streaming with tf32 operands.  A panel is 32 samples (128 B of fp32) of every
             // window row, fetched win_bufs - 1 panels ahead straight to its swizzled place in the
             // hi half of a slot: by ONE TMA tensor copy (a box of 128 B x win_rows rows of the
@@ -1524,7 +1534,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 if (ct == 0) WH_TRACE(7, wcnt);
             }
             if (!tma) asm volatile("cp.async.wait_all;" ::: "memory");
-        } else if (A.pstream) {
+        } else if (PS) {
             // Panel streaming (rows of hop samples).  Each 64-sample column panel of a unit's
             // window (win_rows rows x 256 B of fp32) is copied by cp.async straight into a panel
             // slot, win_bufs - 1 panels ahead; once it has landed the converters read their own
@@ -1670,7 +1680,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 if (ct == 0) WH_TRACE(7, wcnt);
             }
             asm volatile("cp.async.wait_all;" ::: "memory");
-        } else if (A.conv_regs) {
+        } else if (!PS && A.conv_regs) {
             // Register-prefetch path (no staging buffer): each thread loads its first CONV_RC
             // chunks of the next window into registers while the MMAs of the previous unit
             // run, then converts from registers once the window buffer is free.  Larger
@@ -1769,7 +1779,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     window_ready(wb, wcnt);
                 }
             }
-        } else {
+        } else if (!PS) {
         if (A.use_stg && ct == 0 && u0 < n_units) issue(u0);
         uint32_t wcnt = 0;
         for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
@@ -1999,7 +2009,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         for (int64_t item = u0; item < n_units; item += ustride, ++ucnt) {
             int64_t b, tile;
             unit_tile(item, b, tile);
-            if (A.pstream && et == 0) window_prefetch(item + 2 * ustride);  // L2, ahead of the panel copies
+            if (PS && et == 0) window_prefetch(item + 2 * ustride);  // L2, ahead of the panel copies
             const int64_t mrow = tile * 128 + m;  // global row (beyond rows_total: no frames)
             // first frame of this row (rs > 1: only every rs-th row is a frame)
             const int64_t frame0 = A.rs > 1 ? mrow / A.rs : mrow * P;
@@ -2022,19 +2032,19 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const int s0 = pinfo.z & 0xffff, ns = pinfo.z >> 16;
                 if (!WH_DBG(1)) switch (A.output) {
                     case WH_OUT_COMPLEX64:
-                        epi_pass<CC, P, WH_OUT_COMPLEX64>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_COMPLEX64, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_ABS:
-                        epi_pass<CC, P, WH_OUT_ABS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_ABS, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_POWER:
-                        epi_pass<CC, P, WH_OUT_POWER>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_POWER, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_LOG_DB:
-                        epi_pass<CC, P, WH_OUT_LOG_DB>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_LOG_DB, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     default:
-                        epi_pass<CC, P, WH_OUT_LOG1P>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_LOG1P, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                 }
                 // the columns read were re-zeroed; release the buffer to the MMA issuer
@@ -2062,7 +2072,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 }
                 lmin = INFINITY;
                 lmax = -INFINITY;
-                if (A.arrive) {
+                if (VS == 2 && A.arrive) {
                     // all epilogue warps' stores and key atomics of this unit are done: one
                     // arrival per CTA and unit on the clip's counter (release at GPU scope)
                     if (lane == 0) __threadfence();
@@ -2078,7 +2088,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 }
             }
         }
-        if (A.arrive && !A.arrive_only) drain(0);
+        if (VS == 2 && A.arrive && !A.arrive_only) drain(0);
     }
     if (pon && lane == 0) {
         const int role = warp == 0 ? PR_PROD : warp == 1 ? (leader ? PR_MMA : PR_RELAY) : warp < 2 + UM_CONV_WARPS ? PR_CONV : PR_EPI;
@@ -2314,12 +2324,25 @@ __global__ void k_build_bank(BankArgs a) {
 }
 
 using UmmaKernel = void (*)(const UmmaArgs);
+// the kernel variant a plan runs (see k_umma)
+static int umma_variant(const Plan &p) {
+    if (p.pstream) return 1;
+    return (p.norm == WH_NORM_MINMAX && p.minmax_mode != 0) ? 2 : 0;
+}
 
 template <int CC, int CG>
-static UmmaKernel pick_p(int P) {
+static UmmaKernel pick_p(int P, int vs) {
+    if (vs == 1) return P == 1 ? k_umma<CC, 1, CG, 1> : nullptr;  // panel streaming: one frame per row
+    if (vs == 2) {  // opt-in min-max modes (CTA pairs, 1 or 2 phases per row)
+        if constexpr (CG == 2) {
+            if (P == 1) return k_umma<CC, 1, CG, 2>;
+            if (P == 2) return k_umma<CC, 2, CG, 2>;
+        }
+        return nullptr;
+    }
     switch (P) {
-        case 1: return k_umma<CC, 1, CG>;
-        case 2: return k_umma<CC, 2, CG>;
+        case 1: return k_umma<CC, 1, CG, 0>;
+        case 2: return k_umma<CC, 2, CG, 0>;
 #ifdef WH_DEV_BUILD  // development builds (build.py --dev): two phase counts only, a fraction of the compile time
         default: return nullptr;
     }
@@ -2328,18 +2351,18 @@ template <int CC, int CG>
 static UmmaKernel pick_p_unused(int P) {
     switch (P) {
 #endif
-        case 4: return k_umma<CC, 4, CG>;
-        case 8: return k_umma<CC, 8, CG>;
-        case 16: return k_umma<CC, 16, CG>;
-        case 32: return k_umma<CC, 32, CG>;
-        case 64: return k_umma<CC, 64, CG>;
+        case 4: return k_umma<CC, 4, CG, 0>;
+        case 8: return k_umma<CC, 8, CG, 0>;
+        case 16: return k_umma<CC, 16, CG, 0>;
+        case 32: return k_umma<CC, 32, CG, 0>;
+        case 64: return k_umma<CC, 64, CG, 0>;
         default: return nullptr;
     }
 }
 
-static UmmaKernel umma_kernel(int Cc, int P, int CG) {
-    if (CG == 2) return Cc == 2 ? pick_p<2, 2>(P) : pick_p<1, 2>(P);
-    return Cc == 2 ? pick_p<2, 1>(P) : pick_p<1, 1>(P);
+static UmmaKernel umma_kernel(int Cc, int P, int CG, int vs) {
+    if (CG == 2) return Cc == 2 ? pick_p<2, 2>(P, vs) : pick_p<1, 2>(P, vs);
+    return Cc == 2 ? pick_p<2, 1>(P, vs) : pick_p<1, 1>(P, vs);
 }
 
 int umma_supported(const Plan &p, std::string *why) {
@@ -2642,7 +2665,13 @@ static int umma_prepare_impl(Plan &p) {
     int64_t bank_cta = 0;
     for (auto &t : p.tiles) bank_cta += tile_bytes(t);
     // budget known early: the opt-in smem minus static smem and slack (tables added below)
-    UmmaKernel kern0 = umma_kernel(p.Cc, p.P, p.cg);
+    // the opt-in min-max modes exist for CTA pairs with 1 or 2 phases per row (and not with panel
+    // streaming); elsewhere the separate pass
+    if (p.minmax_mode != 0 && (p.pstream || !umma_kernel(p.Cc, p.P, p.cg, 2))) {
+        p.minmax_mode = 0;
+        p.minmax_2pass = true;
+    }
+    UmmaKernel kern0 = umma_kernel(p.Cc, p.P, p.cg, umma_variant(p));
     if (!kern0) return fail(WH_E_UNSUPPORTED, "UMMA engine: unsupported phase count");
     int optin0 = 0;
     cudaDeviceGetAttribute(&optin0, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device);
@@ -2742,7 +2771,7 @@ static int umma_prepare_impl(Plan &p) {
                                  15) / 16 * 16 + 16;  // + one entry of slack: the issue loop reads a tile ahead
     // dynamic smem budget: the opt-in maximum minus the kernel's static smem, the 1 KB
     // alignment slack and the tables
-    UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg);
+    UmmaKernel kern = umma_kernel(p.Cc, p.P, p.cg, umma_variant(p));
     if (!kern) return fail(WH_E_UNSUPPORTED, "UMMA engine: unsupported phase count");
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p.device);
@@ -3076,7 +3105,7 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    WH_CUDA_TRY(cudaLaunchKernelEx(&cfg, umma_kernel(p.Cc, p.P, p.cg), a));
+    WH_CUDA_TRY(cudaLaunchKernelEx(&cfg, umma_kernel(p.Cc, p.P, p.cg, umma_variant(p)), a));
     WH_CUDA_TRY(cudaGetLastError());
     if (a.arrive) {
         FixupArgs f{};

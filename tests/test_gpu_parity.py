@@ -550,6 +550,24 @@ def test_panel_streaming_tf32(hop, tma, monkeypatch):
         np.testing.assert_array_equal(~np.isfinite(got[1, s]), want)
 
 
+@pytest.mark.parametrize("engine,hop", [("umma", 32), ("umma", 1), ("umma", 4), ("simt", 20)])
+def test_complex_magnitude_at_extreme_amplitudes(engine, hop):
+    """|W| of the complex wavelet for clips scaled by 1e-25 and 1e+25: re^2 + im^2 would
+    underflow to 0 / overflow to inf in float32 (the reference computes in float64); the
+    epilogues take the root in a scaled domain, so the rows keep their relative accuracy."""
+    n = 6000 if hop == 1 else 30000
+    x = synth.make_batch(5, clips=3, n=n, start=5)
+    x[1] *= np.float32(1e-25)
+    x[2] *= np.float32(1e25)
+    sc = synth.config_scales(5)[::4] if hop != 32 else synth.config_scales(5)
+    plan = wh.CwthPlan(sc, None, hop, n, wavelet="cmor", output="abs", max_clips=3, engine=engine)
+    got = plan.execute_host(x)
+    plan.close()
+    ref = O.cwth_batch(x, sc, hop, wavelet="cmor", output="abs")
+    assert np.isfinite(got).all() and (got[1].max() > 0)
+    assert row_rel_err(got, ref) <= ROW_TOL
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
 def test_pass_groups_are_byte_identical(groups, monkeypatch):
     """Splitting a tile pair's passes into separate units (what the launcher does when there
