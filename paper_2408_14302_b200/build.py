@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False, dev: b
     # dev (experiments only; never the shipped library): -DWH_DEV_BUILD instantiates two phase counts of the engine
     # kernel instead of seven -- for quick experiments on the large-hop paths
     cflags = [f for f in FLAGS if f != "-shared"] + (["-DWH_DIAG"] if diag else []) + \
-        (["-DWH_DEV_BUILD"] if dev else [])
+        (["-DWH_DEV_BUILD"] if dev else []) + os.environ.get("WH_NVCC_EXTRA", "").split()
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")

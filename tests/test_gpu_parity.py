@@ -568,6 +568,27 @@ def test_complex_magnitude_at_extreme_amplitudes(engine, hop):
     assert row_rel_err(got, ref) <= ROW_TOL
 
 
+@pytest.mark.parametrize("mode", ["inkernel", "concurrent"])
+def test_minmax_modes_fall_back_where_their_kernel_variant_is_absent(mode, monkeypatch):
+    """The opt-in min-max modes live in kernel variants of their own (CTA pairs, 1 or 2 phases
+    per row, no panel streaming); plans of other shapes (hop 16: 4 phases; panel-streamed hop
+    320) take the separate pass and give its bytes."""
+    for hop, n in ((16, 20000), (320, 60000)):
+        x = synth.make_batch(4, clips=3, n=n, start=7)
+        sc = synth.config_scales(4)
+        mk = lambda: wh.CwthPlan(sc, None, hop, n, wavelet="rmor", output="abs", norm="minmax",  # noqa: E731
+                                 max_clips=3, engine="umma")
+        monkeypatch.delenv("WH_UMMA_MINMAX", raising=False)
+        plan = mk()
+        want = plan.execute_host(x).copy()
+        plan.close()
+        monkeypatch.setenv("WH_UMMA_MINMAX", mode)
+        plan = mk()
+        got = plan.execute_host(x)
+        plan.close()
+        assert got.tobytes() == want.tobytes(), (mode, hop)
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
 def test_pass_groups_are_byte_identical(groups, monkeypatch):
     """Splitting a tile pair's passes into separate units (what the launcher does when there
