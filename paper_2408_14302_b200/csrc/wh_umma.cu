@@ -2511,6 +2511,13 @@ static int umma_prepare_impl(Plan &p) {
         // two accumulator sets when (main | corr) fits half a buffer
         p.acc2 = (p.tf32 && 2 * ((cc * (int64_t)p.S + 15) / 16 * 16) <= 128) ? 1 : 0;
         if (const char *t = plan_knob("WH_UMMA_ACC2")) p.acc2 = (p.acc2 && std::atoi(t)) ? 1 : 0;
+        // the row error grows by ~2.5e-8 of the row peak per accumulation step:
+        // tf32 (K = 8 per step) only while an accumulator sees at most ~280 steps (7e-6)
+        if (p.tf32 && 2 * p.Lmax / 8 / (p.acc2 ? 2 : 1) > 280) {
+            p.tf32 = 0;
+            p.acc2 = 0;
+            p.ks = 64;
+        }
     }
     if (!p.pstream) {
         if (p.hop >= 256 && p.hop % 128 != 0) return fail(WH_E_UNSUPPORTED, "UMMA engine: hop needs panel streaming");
