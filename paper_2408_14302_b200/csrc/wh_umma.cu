@@ -2395,6 +2395,14 @@ static UmmaKernel umma_kernel(int Cc, int P, int CG, int vs) {
 
 int umma_supported(const Plan &p, std::string *why) {
     const int64_t H = p.hop;
+    // Accuracy bound: the tensor core's fp32 accumulate truncates, so the row error grows with
+    // the MMAs accumulated into one TMEM accumulator, ~2.5e-8 of the row peak per K = 16 step
+    // (measured: half width 2,661 -> 6.2e-6, 3,990 -> 1.0e-5, 5,322 -> 1.3e-5).  Half widths
+    // beyond 3,360 taps (scale ~650 at the default wavelet) go to the SIMT engine (1.8e-7).
+    if (p.Lmax > 3360) {
+        if (why) *why = "tap support too long for the split-fp16 accumulation within tolerance (half width > 3360)";
+        return WH_E_UNSUPPORTED;
+    }
     const bool small = H <= 64 && 64 % H == 0;
     const bool big = H % 64 == 0 && H < 256;
     const bool strided = H >= 256 && H % 128 == 0;  // rows of 128 samples, every (H/128)-th a frame

@@ -589,6 +589,26 @@ def test_minmax_modes_fall_back_where_their_kernel_variant_is_absent(mode, monke
         assert got.tobytes() == want.tobytes(), (mode, hop)
 
 
+def test_very_long_taps_leave_the_tensor_core_engine():
+    """The split-fp16 accumulation's row error grows with the taps per accumulator (the tensor
+    core's fp32 accumulate truncates): half widths beyond 3,360 taps (scales above ~650) would
+    pass 1e-5, so AUTO takes the SIMT engine there and a forced UMMA plan is refused; scale 600
+    still runs on the tensor cores within tolerance."""
+    n = 100000
+    x = synth.make_batch(5, clips=1, n=n, start=9)
+    for amax, want in ((600.0, "umma"), (1024.0, "simt")):
+        sc = np.geomspace(amax / 4, amax, 6)
+        plan = wh.CwthPlan(sc, None, 32, n, wavelet="cmor", output="abs", max_clips=1, engine="auto")
+        assert plan.engine == want
+        got = plan.execute_host(x)
+        plan.close()
+        ref = O.cwth_batch(x, sc, 32, wavelet="cmor", output="abs")
+        assert row_rel_err(got, ref) <= ROW_TOL, amax
+    with pytest.raises(Exception):
+        wh.CwthPlan(np.geomspace(256.0, 1024.0, 6), None, 32, n, wavelet="cmor", output="abs", max_clips=1,
+                    engine="umma")
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
 def test_pass_groups_are_byte_identical(groups, monkeypatch):
     """Splitting a tile pair's passes into separate units (what the launcher does when there
