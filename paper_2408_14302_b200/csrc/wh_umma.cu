@@ -50,9 +50,6 @@ namespace wh {
 #ifndef WH_CONV_WARPS
 #define WH_CONV_WARPS 6
 #endif
-#ifndef WH_PROD_WARP
-#define WH_PROD_WARP 0  // physical warp of the tap producer (0: roles in physical warp order; 5 measured neutral)
-#endif
 static constexpr int UM_CONV_WARPS = WH_CONV_WARPS;
 static constexpr int UM_CONV_THREADS = 32 * UM_CONV_WARPS;
 static constexpr int UM_EPI_WARPS = 8;  // 2 per TMEM lane quadrant
@@ -820,14 +817,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_decide;  // epilogue: CTA-uniform decision on the oldest pending unit
 
-    // Roles by (virtual) warp: 0 producer, 1 MMA issuer / relay, 2.. converters, then epilogue.
-    // Warp w runs on SM sub-partition w % 4 and the epilogue needs two warps per sub-partition
-    // (TMEM lane quadrant = w % 4); the producer's physical warp is WH_PROD_WARP (with 5 the MMA
-    // issuer's sub-partition fetches the two small loops and the epilogue, no converter code:
-    // measured neutral, c2 62.4 vs 62.5 us, c5 978 vs 976 us)
-    const int pwarp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int warp = pwarp == 0 ? WH_PROD_WARP : (pwarp == WH_PROD_WARP ? 0 : pwarp);
-    const int vtid = warp * 32 + lane;  // thread index in role order
+    // Roles by warp: 0 producer, 1 MMA issuer / relay, 2.. converters, then epilogue (two warps
+    // per TMEM lane quadrant = SM sub-partition).  (The producer on the MMA issuer's
+    // sub-partition instead of warp 0's measured neutral: c2 62.4 vs 62.5 us, c5 978 vs 976 us.)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (kDiag && A.trace && threadIdx.x == 0 && blockIdx.x < 256) {
         A.trace[16 * 32 + 2 * blockIdx.x] = (long long)globaltimer_ns();
         if (blockIdx.x == 0) A.trace[14 * 32] = clock64();  // SM clock rate = cycles / ns
@@ -883,7 +876,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const int32_t in_lo = (int32_t)(w0 < 0 ? -w0 : 0);
         const int64_t in_hi64 = A.N - w0;
         const int32_t in_hi = (int32_t)(in_hi64 < (int64_t)0x7fffffff ? in_hi64 : (int64_t)0x7fffffff);
-        const int ct = vtid - 64, chunks = A.win_rows * A.panels * 8;
+        const int ct = (int)threadIdx.x - 64, chunks = A.win_rows * A.panels * 8;
         auto chunk_off = [&](int c) {
             int row, cc;
             chunk_rc(A, c, row, cc);
@@ -963,7 +956,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const uintptr_t a1 = (reinterpret_cast<uintptr_t>(A.x + b * A.ld_x + hi) + 15) & ~(uintptr_t)15;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
     };
-    if (vtid == 64)
+    if (threadIdx.x == 64)
         for (int k = 1; k <= UM_PF; ++k) window_prefetch(u0 + k * ustride);
     constexpr int PS = VS == 1 ? 1 : 0;  // panel streaming
     if (warp >= 2 && warp < 2 + UM_CONV_WARPS && A.conv_regs && u0 < n_units) conv_fetch(u0);
@@ -1330,7 +1323,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         // ===================== converters ============================================
         // The fp32 window of a tile is a contiguous sample range of the clip; one elected
         // converter thread bulk-copies it into the staging buffer one unit ahead.
-        const int ct = vtid - 64;  // 0 .. UM_CONV_THREADS-1
+        const int ct = (int)threadIdx.x - 64;  // 0 .. UM_CONV_THREADS-1
         // window wb of unit wcnt is converted (all converter threads passed bar 1): tell the
         // MMA issuer -- the leader's own barrier, directly from the peer CTA too
         auto window_ready = [&](uint32_t wb, uint32_t wcnt) {
@@ -1934,7 +1927,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         const int quad = warp & 3;          // TMEM lanes 32*quad .. 32*quad+31
         const int half = (warp - 2 - UM_CONV_WARPS) >> 2;  // which 16-column units
         const int m = quad * 32 + lane;     // row within the tile
-        const int et = vtid - (64 + UM_CONV_THREADS);  // 0 .. 255
+        const int et = (int)threadIdx.x - (64 + UM_CONV_THREADS);  // 0 .. 255
         const bool vec = A.out_vec_ok;
         uint32_t acnt = 0, ucnt = 0;
         float lmin = INFINITY, lmax = -INFINITY;
