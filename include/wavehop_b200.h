@@ -73,8 +73,8 @@ enum { WH_NORM_NONE = 0, WH_NORM_MINMAX = 1, WH_NORM_RENDER_U8 = 2, WH_NORM_REND
 
 /* Compute engine.  AUTO picks the tcgen05 split-fp16 engine when the hop allows a
  * polyphase tiling (hop dividing 64 or 192, hop 128, or a multiple of 64 from 256), the plan
- * fits shared memory and the longest filter's half width is at most 3,360 taps (the accuracy
- * bound of the split-fp16 accumulation), else the SIMT fp32 engine; UMMA forced on a plan it
+ * fits shared memory and the longest filter's half width is at most 3,360 taps (5,632 at hops
+ * 16 / 32 / 64: the accuracy bounds of the split-fp16 accumulation), else the SIMT fp32 engine; UMMA forced on a plan it
  * cannot run returns WH_E_UNSUPPORTED.  There is no CPU engine. */
 enum { WH_ENGINE_AUTO = 0, WH_ENGINE_SIMT = 1, WH_ENGINE_UMMA = 2 };
 

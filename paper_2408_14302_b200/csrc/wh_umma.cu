@@ -61,6 +61,13 @@ static constexpr int UM_CONV_RC = 40 / UM_CONV_WARPS;  // register-prefetch conv
 static constexpr int UM_WSLOTS = 4; // window buffers (panel streaming: panel slots; otherwise <= 2 used)
 static constexpr int UM_SEG = 8192; // panel streaming: samples per pre-pass max segment
 static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
+// Accuracy bounds on the longest filter's half width (taps): the tensor core's fp32 accumulate
+// truncates, so the row error grows with the MMAs accumulated into one TMEM accumulator, about
+// 2.5e-8 of the row peak per K = 16 step (measured: half width 2,661 -> 6.2e-6, 3,990 ->
+// 1.0e-5, 5,322 -> 1.3e-5).  Up to UM_LMAX1 one accumulator set; up to UM_LMAX2 two sets per
+// buffer that the epilogue adds (kernel variant 3, passes of 64 columns: 3,990 -> 5.0e-6,
+// 5,322 -> 6.2e-6, 6,651 -> 1.0e-5); beyond: SIMT engine.
+static constexpr int64_t UM_LMAX1 = 3360, UM_LMAX2 = 5632;
 
 // Diagnostics (role switches, per-role wait counters, the CTA-0 timeline) exist only in a
 // build with -DWH_DIAG (paper_2408_14302_b200/build.py --diag); the product build compiles
@@ -959,6 +966,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     if (threadIdx.x == 64)
         for (int k = 1; k <= UM_PF; ++k) window_prefetch(u0 + k * ustride);
     constexpr int PS = VS == 1 ? 1 : 0;  // panel streaming
+    constexpr int AC = (VS == 1 || VS == 3) ? 1 : 0;  // two accumulator sets per buffer possible
     if (warp >= 2 && warp < 2 + UM_CONV_WARPS && A.conv_regs && u0 < n_units) conv_fetch(u0);
     const uint32_t WH = A.win_half_bytes;               // bytes of one (hi or lo) window
     uint8_t *win_base = smem;                            // [win_bufs][hi|lo][panels][rows][128]
@@ -1266,17 +1274,21 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         const uint32_t ah = a_hi16 + (tt.x & 0xffffu), al = ah + wh16;
                         const uint32_t b1 = g16 + (tt.y & 0xffffu), b2 = b1 + (tt.y >> 16);
                         const uint32_t d1 = d_acc + (tt.x >> 16), d2 = d_acc + C;
+                        // VS = 3 (very long filters): odd K-slices go to the second accumulator set
+                        // of the buffer, 128 columns on (half the accumulation steps per set)
+                        constexpr uint32_t o2 = VS == 3 ? 128u : 0u;
                         if (!WH_DBG(4) && elect_one()) {
                             if (tt.w) {
 #pragma unroll
                                 for (uint32_t j = 0; j < 4; ++j) {
-                                    umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
-                                    umma_f16<CG>(d2, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
+                                    const uint32_t o = (j & 1) ? o2 : 0u;
+                                    umma_f16<CG>(d1 + o, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                                    umma_f16<CG>(d2 + o, DESC_HI | (al + 2 * j), DESC_HI | (b2 + 2 * j), tt.w);
                                 }
                             } else {
 #pragma unroll
                                 for (uint32_t j = 0; j < 4; ++j)
-                                    umma_f16<CG>(d1, DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
+                                    umma_f16<CG>(d1 + ((j & 1) ? o2 : 0u), DESC_HI | (ah + 2 * j), DESC_HI | (b1 + 2 * j), tt.z);
                             }
                         }
                         __syncwarp();
@@ -2053,19 +2065,19 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const int s0 = pinfo.z & 0xffff, ns = pinfo.z >> 16;
                 if (!WH_DBG(1)) switch (A.output) {
                     case WH_OUT_COMPLEX64:
-                        epi_pass<CC, P, WH_OUT_COMPLEX64, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_COMPLEX64, AC>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_ABS:
-                        epi_pass<CC, P, WH_OUT_ABS, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_ABS, AC>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_POWER:
-                        epi_pass<CC, P, WH_OUT_POWER, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_POWER, AC>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     case WH_OUT_LOG_DB:
-                        epi_pass<CC, P, WH_OUT_LOG_DB, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_LOG_DB, AC>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                     default:
-                        epi_pass<CC, P, WH_OUT_LOG1P, PS>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
+                        epi_pass<CC, P, WH_OUT_LOG1P, AC>(A, s_spow, tbase, cbase, s0, ns, pinfo.w, half, b, frame0, nvalid, e, vec, lmin, lmax);
                         break;
                 }
                 // the columns read were re-zeroed; release the buffer to the MMA issuer
@@ -2348,6 +2360,7 @@ using UmmaKernel = void (*)(const UmmaArgs);
 // the kernel variant a plan runs (see k_umma)
 static int umma_variant(const Plan &p) {
     if (p.pstream) return 1;
+    if (p.Lmax > UM_LMAX1) return 3;
     return (p.norm == WH_NORM_MINMAX && p.minmax_mode != 0) ? 2 : 0;
 }
 
@@ -2358,6 +2371,16 @@ static UmmaKernel pick_p(int P, int vs) {
         if constexpr (CG == 2) {
             if (P == 1) return k_umma<CC, 1, CG, 2>;
             if (P == 2) return k_umma<CC, 2, CG, 2>;
+        }
+        return nullptr;
+    }
+    if (vs == 3) {  // very long filters: two accumulator sets per buffer (CTA pairs, 1 / 2 / 4 phases per row)
+        if constexpr (CG == 2) {
+            if (P == 1) return k_umma<CC, 1, CG, 3>;
+            if (P == 2) return k_umma<CC, 2, CG, 3>;
+#ifndef WH_DEV_BUILD
+            if (P == 4) return k_umma<CC, 4, CG, 3>;
+#endif
         }
         return nullptr;
     }
@@ -2388,12 +2411,13 @@ static UmmaKernel umma_kernel(int Cc, int P, int CG, int vs) {
 
 int umma_supported(const Plan &p, std::string *why) {
     const int64_t H = p.hop;
-    // Accuracy bound: the tensor core's fp32 accumulate truncates, so the row error grows with
-    // the MMAs accumulated into one TMEM accumulator, ~2.5e-8 of the row peak per K = 16 step
-    // (measured: half width 2,661 -> 6.2e-6, 3,990 -> 1.0e-5, 5,322 -> 1.3e-5).  Half widths
-    // beyond 3,360 taps (scale ~650 at the default wavelet) go to the SIMT engine (1.8e-7).
-    if (p.Lmax > 3360) {
-        if (why) *why = "tap support too long for the split-fp16 accumulation within tolerance (half width > 3360)";
+    // (accuracy bounds: UM_LMAX1 / UM_LMAX2)
+    if (p.Lmax > UM_LMAX2) {
+        if (why) *why = "tap support too long for the split-fp16 accumulation within tolerance (half width > 5632)";
+        return WH_E_UNSUPPORTED;
+    }
+    if (p.Lmax > UM_LMAX1 && !(H <= 64 && 64 % H == 0 && 64 / H <= 4)) {
+        if (why) *why = "very long filters (half width > 3360) run on the tensor cores for hops 16, 32 and 64 only";
         return WH_E_UNSUPPORTED;
     }
     const bool small = H <= 64 && 64 % H == 0;
@@ -2542,7 +2566,8 @@ static int umma_prepare_impl(Plan &p) {
         // serves twice the columns (c4 hop 64, 64 scales: 285 -> 228 us, the bank streamed
         // beside two windows); with more columns the second pass re-reads A (c2: 65 -> 110 us)
         const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
-        p.doubled_v = p.rs == 1 && !p.pstream && 2 * p.V <= 256 && 2 * (p.V / H) * cc * (int64_t)p.S <= 128 && !p.no_2v &&
+        const int64_t colcap = p.Lmax > UM_LMAX1 ? 64 : 128;  // columns of a pass
+        p.doubled_v = p.rs == 1 && !p.pstream && 2 * p.V <= 256 && 2 * (p.V / H) * cc * (int64_t)p.S <= colcap && !p.no_2v &&
                       plan_knob("WH_UMMA_V") == nullptr && plan_knob("WH_UMMA_NO_2V") == nullptr;
         if (p.doubled_v) p.V *= 2;
     }
@@ -2572,7 +2597,14 @@ static int umma_prepare_impl(Plan &p) {
     if (const char *t = plan_knob("WH_UMMA_TAU")) tau_log2 = std::atoi(t);
     // TMEM: 512 columns = 2 accumulator buffers x (128 main + 128 correction) columns, so a
     // pass covers at most 128 columns and the epilogue of pass n overlaps the MMAs of n+1.
-    const int max_cols = 128;
+    const bool longf = p.Lmax > UM_LMAX1;  // two accumulator sets per buffer: passes of 64 columns
+    if (longf) {
+        if (p.pstream) return fail(WH_E_UNSUPPORTED, "UMMA engine: very long filters are not panel-streamed");
+        p.acc2 = 1;
+        p.minmax_mode = 0;
+        p.minmax_2pass = true;
+    }
+    const int max_cols = longf ? 64 : 128;
     p.n_acc = 2;
     p.acc_stride = 256;
     int win_bufs = 0, bstages = 0;

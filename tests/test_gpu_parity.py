@@ -589,24 +589,33 @@ def test_minmax_modes_fall_back_where_their_kernel_variant_is_absent(mode, monke
         assert got.tobytes() == want.tobytes(), (mode, hop)
 
 
-def test_very_long_taps_leave_the_tensor_core_engine():
+def test_very_long_taps():
     """The split-fp16 accumulation's row error grows with the taps per accumulator (the tensor
-    core's fp32 accumulate truncates): half widths beyond 3,360 taps (scales above ~650) would
-    pass 1e-5, so AUTO takes the SIMT engine there and a forced UMMA plan is refused; scale 600
-    still runs on the tensor cores within tolerance."""
-    n = 100000
+    core's fp32 accumulate truncates).  Half widths beyond 3,360 taps (scales above ~650) run
+    with two accumulator sets per buffer (kernel variant 3, hops 16 / 32 / 64); beyond 5,632
+    (scale ~1,080) -- or at other hops -- AUTO takes the SIMT engine and a forced UMMA plan is
+    refused.  Every case within the row tolerance."""
+    n = 48000
     x = synth.make_batch(5, clips=1, n=n, start=9)
-    for amax, want in ((600.0, "umma"), (1024.0, "simt")):
-        sc = np.geomspace(amax / 4, amax, 6)
-        plan = wh.CwthPlan(sc, None, 32, n, wavelet="cmor", output="abs", max_clips=1, engine="auto")
-        assert plan.engine == want
+    for amax, hop, want in ((600.0, 32, "umma"), (1024.0, 32, "umma"), (1024.0, 64, "umma"), (1024.0, 16, "umma"),
+                            (1024.0, 128, "simt"), (1400.0, 32, "simt")):
+        sc = np.geomspace(amax / 4, amax, 4)
+        plan = wh.CwthPlan(sc, None, hop, n, wavelet="cmor", output="abs", max_clips=1, engine="auto")
+        assert plan.engine == want, (amax, hop)
         got = plan.execute_host(x)
         plan.close()
-        ref = O.cwth_batch(x, sc, 32, wavelet="cmor", output="abs")
-        assert row_rel_err(got, ref) <= ROW_TOL, amax
+        ref = O.cwth_batch(x, sc, hop, wavelet="cmor", output="abs")
+        assert row_rel_err(got, ref) <= ROW_TOL, (amax, hop)
     with pytest.raises(Exception):
-        wh.CwthPlan(np.geomspace(256.0, 1024.0, 6), None, 32, n, wavelet="cmor", output="abs", max_clips=1,
+        wh.CwthPlan(np.geomspace(350.0, 1400.0, 4), None, 32, n, wavelet="cmor", output="abs", max_clips=1,
                     engine="umma")
+    # min-max on a long-filter plan (the separate pass) and a real wavelet
+    sc = np.geomspace(256.0, 1024.0, 3)
+    plan = wh.CwthPlan(sc, None, 32, n, wavelet="rmor", output="abs", norm="minmax", max_clips=1, engine="umma")
+    got = plan.execute_host(x)
+    plan.close()
+    ref = O.cwth_batch(x, sc, 32, wavelet="rmor", output="abs", norm="minmax")
+    check_minmax(got, ref, O.cwth_batch(x, sc, 32, wavelet="rmor", output="abs"), "abs")
 
 
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])

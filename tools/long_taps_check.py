@@ -10,7 +10,7 @@ from paper_2408_14302_b200 import synth  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
 x = synth.make_batch(5, clips=1, n=120000, start=3)
-for amax in (512, 768, 1024, 1400):
+for amax in (512, 768, 1024, 1280, 1400):
     sc = np.geomspace(amax / 8, amax, 12)
     for engine in ("umma", "simt"):
         try:
