@@ -17,17 +17,22 @@
 //   resident in shared memory when it fits, else streamed per tap group with cp.async.bulk.
 //   Precision: x*2^e = xh + xl, t*2^f = th + tl (fp16 each); main += xh*th and, in a
 //   separate accumulator, corr += xh*tl + xl*th (fp32, TMEM); the cross terms are skipped
-//   on tap tails below 2^-12 of the scale's peak; W = (main + corr) * 2^-(e+f).
+//   on tap tails below 2^-8 of the scale's peak; W = (main + corr) * 2^-(e+f).
 //
-// CTA roles (448 threads, 1 CTA per SM, CTA pairs (cta_group::2, M = 256), persistent over
-// units = (clip, pair of 128-row tiles)):
+// CTA roles (512 threads, 1 CTA per SM, CTA pairs (cta_group::2, M = 256), persistent over
+// units = (clip, pair of 128-row tiles, group of passes)):
 //   warp 0      producer: cp.async.bulk of the resident bank / streamed tap groups
 //   warp 1      leader CTA: TMEM allocator + MMA issuer (one elected thread);
 //               peer CTA: relays "tap group landed" to the leader's barriers
-//   warps 2-5   converters: window -> registers -> max -> exponent -> hi/lo fp16, stored
+//   warps 2-7   converters: window -> registers -> max -> exponent -> hi/lo fp16, stored
 //               swizzled once the window buffer is free
-//   warps 6-13  epilogue (2 per TMEM lane quadrant): tcgen05.ld main + corr -> scale,
+//   warps 8-15  epilogue (2 per TMEM lane quadrant): tcgen05.ld main + corr -> scale,
 //               |W| / power / log_db / log1p -> 16-byte global stores, per-clip min/max
+//
+// Kernel variants k_umma<CC, P, CG, VS>: VS = 0 the common engine; 1 panel streaming (rows of
+// hop samples for hops >= 256: fp16 split with a pre-pass, or tf32 operands fetched by TMA
+// tensor copies); 2 the opt-in per-clip min-max arrival modes; 3 very long filters (two
+// accumulator sets per TMEM buffer).  Each variant's extra code is compiled only there.
 #include <cuda.h>  // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint: no libcuda link)
 #include <cuda_fp16.h>
 #include <math.h>
