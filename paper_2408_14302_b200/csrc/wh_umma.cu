@@ -1585,26 +1585,80 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             const uint32_t NS = (uint32_t)A.win_bufs;
             // cp.async of panel (item, p) into slot `sl`: chunk c of this thread = row c >> 3,
             // 8 samples at column (c & 7) * 8; out-of-clip samples are stored as zeros
-            auto fetch_panel = [&](int64_t item, int p, uint32_t sl) {
+            // Fetch geometry of a unit, computed once per unit: this thread's chunk i sits at window
+            // row (ct >> 3) + i * CONV_THREADS / 8, samples (ct & 7) * 8 .. + 7 of the panel; for a
+            // window inside the clip the copies advance by fixed steps with no per-chunk tests.
+            struct FGeo {
+                const float *xb;
+                int64_t g0;      // clip sample of this thread's first chunk in panel 0
+                int64_t r0;      // tma: tensor row of the window's first row (floor(w0 / V))
+                int32_t coff;    // tma: column of the window's first sample in that row
+                int32_t b;
+                bool interior;
+                bool tail;       // tma: the window reaches the clip's last, partial row of V samples
+            };
+            auto fgeo = [&](int64_t item) {
+                FGeo g;
                 int64_t b, tile;
                 unit_tile(item, b, tile);
                 const int64_t w0 = tile * 128 * A.V - A.G0;
-                const float *xb = A.x + b * A.ld_x;
-                float *dst = reinterpret_cast<float *>(win_base + (size_t)sl * 2 * WH);
+                g.xb = A.x + b * A.ld_x;
+                g.g0 = w0 + (int64_t)(ct >> 3) * A.V + (ct & 7) * 8;
+                const int64_t wend = w0 + (int64_t)A.win_rows * A.V;
+                g.interior = A.vec_ok && w0 >= 0 && wend <= A.N;
+                g.tail = A.full_end < A.N && wend > A.full_end;
+                g.b = (int32_t)b;
+                const int64_t q = (int64_t)((uint32_t)A.G0 / (uint32_t)A.V);
+                const int32_t rem = A.G0 - (int32_t)q * A.V;
+                g.r0 = tile * 128 - q - (rem ? 1 : 0);
+                g.coff = rem ? A.V - rem : 0;
+                return g;
+            };
+            const bool tma = A.tma != 0;  // panels by one TMA tensor copy each (plain rows of 256 B)
+            constexpr int FRS = UM_CONV_THREADS / 8;  // rows between a thread's chunks
+            const int64_t fgstep = (int64_t)FRS * A.V;
+            const int fmine = ct < pchunks ? (pchunks - ct + UM_CONV_THREADS - 1) / UM_CONV_THREADS : 0;
+            const uint32_t fdst0 = smem_u32(win_base) + (uint32_t)(ct >> 3) * 256u + (uint32_t)(ct & 7) * 32u;
+            auto fetch_panel = [&](const FGeo &g, int p, uint32_t sl) {
+                if (tma) {
+                    if (ct == 0) {
+                        int64_t r0 = g.r0;
+                        int32_t col = g.coff + p * 64;
+                        if (col >= A.V) {
+                            col -= A.V;
+                            ++r0;
+                        }
+                        mbar_expect_tx(&slot_full[sl], 2 * WH);
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                            "{%2, %3, %4}], [%5];" ::"r"(smem_u32(win_base) + sl * 2 * WH),
+                            "l"(&A.tmap), "r"(col), "r"((int32_t)r0), "r"(g.b), "r"(smem_u32(&slot_full[sl]))
+                            : "memory");
+                    }
+                    return;
+                }
+                uint32_t dst = fdst0 + sl * 2 * WH;
+                if (g.interior) {
+                    const float *src = g.xb + g.g0 + p * 64;
+                    for (int i = 0; i < fmine; ++i, dst += FRS * 256u, src += fgstep) {
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(src + 4) : "memory");
+                    }
+                } else {
+                    int64_t q = g.g0 + p * 64;
+                    for (int i = 0; i < fmine; ++i, dst += FRS * 256u, q += fgstep) {
+                        if (A.vec_ok && q >= 0 && q + 8 <= A.N) {
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g.xb + q) : "memory");
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(g.xb + q + 4) : "memory");
+                        } else {
+                            float z[8];
 #pragma unroll
-                for (int i = 0; i < PCH; ++i) {
-                    const int c = ct + i * UM_CONV_THREADS;
-                    if (c >= pchunks) continue;
-                    const int row = c >> 3;
-                    const int64_t g = w0 + (int64_t)row * A.V + p * 64 + (c & 7) * 8;  // clip sample
-                    float *d = dst + row * 64 + (c & 7) * 8;
-                    if (A.vec_ok && g >= 0 && g + 8 <= A.N) {
-                        const uint32_t sa = smem_u32(d);
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(xb + g) : "memory");
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16), "l"(xb + g + 4) : "memory");
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) d[k] = (g + k >= 0 && g + k < A.N) ? __ldg(xb + g + k) : 0.0f;
+                            for (int k = 0; k < 8; ++k) z[k] = (q + k >= 0 && q + k < A.N) ? __ldg(g.xb + q + k) : 0.0f;
+                            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(z[0]), "f"(z[1]),
+                                         "f"(z[2]), "f"(z[3]) : "memory");
+                            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16), "f"(z[4]), "f"(z[5]),
+                                         "f"(z[6]), "f"(z[7]) : "memory");
+                        }
                     }
                 }
                 asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1614,21 +1668,26 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
             int64_t f_item = u0;
             int f_p = 0;
             uint32_t fc = 0;  // panels fetched so far
+            FGeo fg = fgeo(u0 < n_units ? u0 : 0);
             auto fetch_next = [&]() {
-                if (f_item < n_units) fetch_panel(f_item, f_p, fc % NS);
-                else asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+                if (f_item < n_units) fetch_panel(fg, f_p, fc % NS);
+                else if (!tma) asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
                 ++fc;
                 if (++f_p == A.panels) {
                     f_p = 0;
                     f_item += ustride;
+                    if (f_item < n_units) fg = fgeo(f_item);
                 }
             };
-            for (uint32_t j = 0; j + 1 < NS; ++j) fetch_next();
+            const uint32_t lag = tma ? 2u : 1u;  // TMA copies run NS - 2 panels ahead (their slot was released long ago)
+            for (uint32_t j = 0; j + lag < NS; ++j) fetch_next();
             uint32_t qc = 0, wcnt = 0;
             for (int64_t item = u0; item < n_units; item += ustride, ++wcnt) {
                 int64_t b, tile;
                 unit_tile(item, b, tile);
                 const int64_t w0 = tile * 128 * A.V - A.G0;
+                const bool utail = tma && A.full_end < A.N && w0 + (int64_t)A.win_rows * A.V > A.full_end;
+                const float *uxb = A.x + b * A.ld_x;
                 int p0, p1;
                 unit_passes(item, p0, p1);
                 const int64_t own0 = tile * 128 * A.V, own1 = own0 + 128 * (int64_t)A.V;
@@ -1651,10 +1710,11 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 for (int p = 0; p < A.panels; ++p, ++qc) {
                     const uint32_t sl = qc % NS;
                     float *src = reinterpret_cast<float *>(win_base + (size_t)sl * 2 * WH);
-                    // this panel's copies (this thread's own) have landed
+                    // this panel's copies (this thread's own, or the TMA copy) have landed
                     {
                         const long long tw = pon ? clock64() : 0;
-                        asm volatile("cp.async.wait_group %0;" ::"n"(UM_WSLOTS - 2) : "memory");
+                        if (tma) mbar_wait(&slot_full[sl], (qc / NS) & 1);
+                        else asm volatile("cp.async.wait_group %0;" ::"n"(UM_WSLOTS - 2) : "memory");
                         if (pon) pa.c[0] += (unsigned long long)(clock64() - tw);
                     }
                     float pv[PCH][8];
@@ -1666,6 +1726,15 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                         const float4 u = q[0], w = q[1];
                         float (&v)[8] = pv[i];
                         v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
+                        if (utail) {
+                            // the clip's last row of V samples is partial: the tensor ends before it
+                            // (zero fill), its samples come straight from the clip
+                            const int64_t g = w0 + (int64_t)(c >> 3) * A.V + p * 64 + (c & 7) * 8;
+                            if (g >= A.full_end && g < A.N) {
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) v[k] = g + k < A.N ? __ldg(uxb + g + k) : 0.0f;
+                            }
+                        }
                         float m = 0.0f;
 #pragma unroll
                         for (int k = 0; k < 8; ++k) m = fmax_nan(m, fabsf(v[k]));
@@ -1708,16 +1777,17 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     asm volatile("bar.sync 1, %0;" ::"r"(UM_CONV_THREADS) : "memory");
                     if (ct == 0) window_ready(sl, qc);
-                    // refill the slot of the previous panel once its MMAs are done
-                    if (qc >= 1) {
-                        const uint32_t ps = (qc - 1) % NS;
-                        mbar_wait_p(&win_empty[ps], ((qc - 1) / NS) & 1, pa, 1, pon);
+                    // refill the slot of an earlier panel once its MMAs are done (TMA: only the
+                    // issuing thread waits)
+                    if (qc >= lag && (!tma || ct == 0)) {
+                        const uint32_t ps = (qc - lag) % NS;
+                        mbar_wait_p(&win_empty[ps], ((qc - lag) / NS) & 1, pa, 1, pon);
                     }
                     fetch_next();
                 }
                 if (ct == 0) WH_TRACE(7, wcnt);
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
+            if (!tma) asm volatile("cp.async.wait_all;" ::: "memory");
         } else if (!PS && A.conv_regs) {
             // Register-prefetch path (no staging buffer): each thread loads its first CONV_RC
             // chunks of the next window into registers while the MMAs of the previous unit
@@ -2516,6 +2586,7 @@ static int umma_prepare_impl(Plan &p) {
     // + halo rows of hop samples) is too large to hold whole, so it streams through two
     // panel slots in 64-sample column panels, the K-steps in panel-major order, the tap bank
     // resident; the window's exponent is computed one unit ahead (epilogue warps).
+    p.no_tma = plan_knob("WH_UMMA_NO_TMA") != nullptr;
     {
         const int64_t cc = p.wavelet == WH_WAVELET_CMOR ? 2 : 1;
         // measured slower than rows of 128 on c4 (hop 256 / 1024: 214 / 241 vs 205 / 205 us, 6
@@ -2537,7 +2608,6 @@ static int umma_prepare_impl(Plan &p) {
         if (p.pstream)
             if (const char *t = plan_knob("WH_UMMA_TF32")) p.tf32 = std::atoi(t) ? 1 : 0;
         p.ks = p.tf32 ? 32 : 64;
-        p.no_tma = plan_knob("WH_UMMA_NO_TMA") != nullptr;
         // two accumulator sets when (main | corr) fits half a buffer
         p.acc2 = (p.tf32 && 2 * ((cc * (int64_t)p.S + 15) / 16 * 16) <= 128) ? 1 : 0;
         if (const char *t = plan_knob("WH_UMMA_ACC2")) p.acc2 = (p.acc2 && std::atoi(t)) ? 1 : 0;
@@ -3110,17 +3180,20 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.acc2 = p.acc2;
     a.full_end = (p.N / p.V) * p.V;
     a.tma = 0;
-    if (p.tf32 && !p.no_tma && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ld_x % 4 == 0 && p.N >= p.V &&
+    if (p.pstream && !p.no_tma && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ld_x % 4 == 0 && p.N >= p.V &&
         p.win_rows <= 256 && clips <= 0x7fffffff && encode_tiled()) {
         // the batch as (V samples, N / V whole rows, clips): a window panel is one box of
         // 32 samples x win_rows rows; rows before / after the clip's whole rows are zero-filled
         const cuuint64_t dims[3] = {(cuuint64_t)p.V, (cuuint64_t)(p.N / p.V), (cuuint64_t)clips};
         const cuuint64_t strides[2] = {(cuuint64_t)p.V * 4, (cuuint64_t)ld_x * 4};
-        const cuuint32_t box[3] = {32, (cuuint32_t)p.win_rows, 1};
+        // tf32: 32-sample panels straight into the 128 B-swizzled operand layout; fp16: 64-sample
+        // panels as plain rows of 256 B that the converters split
+        const cuuint32_t box[3] = {p.tf32 ? 32u : 64u, (cuuint32_t)p.win_rows, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         const CUresult r = encode_tiled()(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(x), dims,
                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                          p.tf32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         a.tma = r == CUDA_SUCCESS ? 1 : 0;
     }

@@ -87,7 +87,7 @@ for i in range(n_cases):
         ok = sc > 0
         err = float((np.abs(g2[ok] - r2[ok]).max(axis=1) / sc[ok]).max()) if ok.any() else float(np.abs(g2).max())
         tol = 2e-5 if output == "power" else 1e-5
-    worst = max(worst, err / tol)
+    worst = max(worst, err / tol if tol > 0 else (0.0 if err == 0 else float("inf")))  # (constant clip: tol 0, err 0)
     if not err <= tol:
         print("FAIL (tolerance)", case, f"err {err:.3e} tol {tol:.1e}", flush=True)
         sys.exit(1)
