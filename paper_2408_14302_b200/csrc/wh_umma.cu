@@ -2594,7 +2594,28 @@ static int umma_prepare_impl(Plan &p) {
         // of one CTA per tile while a clip's last tile (29 of 157 frames at hop 1024) leaves its
         // pair partner idle; used where rows of 128 cannot be (hops that are multiples of 64
         // but not of 128) and on request (WH_UMMA_PSTREAM=1)
-        const bool want = plan_knob("WH_UMMA_PSTREAM") != nullptr || H % 128 != 0;
+        // Hops that are multiples of 128 can also run as rows of 128 samples (every (hop/128)-th
+        // row a frame): the cheaper of the two by a model fitted to c4-shaped batches (cycles at
+        // ~1.7 GHz; profiles/r02k_hops.txt): a unit (pair of 128-row tiles) costs its K-steps'
+        // MMAs -- ~620 cycles per K-step panel-streamed, ~430 in rows of 128 -- or, panel-streamed,
+        // its panels' conversion (~30 cycles per window row and panel) if that is longer, plus the
+        // pre-pass over the input; units run in rounds over the CTA pairs.  Panel streaming must
+        // model 5 % cheaper to be taken.
+        bool model_ps = false;
+        if (H % 128 == 0 && H >= 256) {
+            const double ksteps = (double)((2 * p.Lmax + 64) / 64 + 1);
+            const double pairs = std::max(1, p.sms / 2), clips = (double)std::max<int64_t>(1, p.max_clips);
+            const int64_t tiles_ps = (p.F + 127) / 128, rows128 = (p.F - 1) * (H / 128) + 1;
+            const int64_t tiles_128 = (rows128 + 127) / 128;
+            const double rounds_ps = std::ceil(clips * (double)((tiles_ps + 1) / 2) / pairs);
+            const double rounds_128 = std::ceil(clips * (double)((tiles_128 + 1) / 2) / pairs);
+            const double win_rows = 128.0 + (double)(2 * p.Lmax / H) + 8.0;
+            const double t_ps = rounds_ps * std::max(620.0 * ksteps, 30.0 * win_rows * (double)(H / 64)) +
+                                clips * (double)p.N * 1.05e-3;
+            const double t_128 = rounds_128 * 430.0 * ksteps;
+            model_ps = t_ps < 0.95 * t_128;
+        }
+        const bool want = plan_knob("WH_UMMA_PSTREAM") != nullptr || H % 128 != 0 || model_ps;
         p.pstream = (!p.no_pstream && want && plan_knob("WH_UMMA_NO_PSTREAM") == nullptr && H >= 256 &&
                      H <= 4096 && H % 64 == 0 && cc * (int64_t)p.S <= 128) ? 1 : 0;
         // tf32 operands (kind::tf32, K-steps of 32 taps): the fp32 samples are split in place
