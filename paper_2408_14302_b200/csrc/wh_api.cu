@@ -328,7 +328,7 @@ static void plan_free(Plan *p) {
     cudaFree(p->d_fold); cudaFree(p->d_scales); cudaFree(p->d_half); cudaFree(p->d_fold_off);
     cudaFree(p->d_groups); cudaFree(p->d_items); cudaFree(p->d_group_taps);
     cudaFree(p->d_passes); cudaFree(p->d_tiles); cudaFree(p->d_groups_u); cudaFree(p->d_bank); cudaFree(p->d_scale_pow); cudaFree(p->d_tables);
-    cudaFree(p->d_minmax); cudaFree(p->d_nfbad); cudaFree(p->d_nfctl); cudaFree(p->d_segmax); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
+    cudaFree(p->d_minmax); cudaFree(p->d_nfbad); cudaFree(p->d_nfctl); cudaFree(p->d_arrive); cudaFree(p->d_abandon); cudaFree(p->d_scratch); cudaFree(p->d_rparams); cudaFree(p->d_x); cudaFree(p->d_out); cudaFree(p->d_prof); cudaFree(p->d_trace);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     if (p->nstream) cudaStreamDestroy(p->nstream);

@@ -171,7 +171,6 @@ struct Plan {
     // record their positions; a fix-up then writes the exact IEEE value of every coefficient
     // whose support contains one (the reference's propagation, wavelet.py:264-270)
     uint32_t *d_nfbad = nullptr;   // [max_clips][1 + WH_NF_CAP]: count, positions
-    float *d_segmax = nullptr;     // UMMA panel streaming: per-segment max |x| [max_clips][nseg]
     uint32_t *d_nfctl = nullptr;   // [max_clips][2]: per-launch CTA counter (slot of the launch's first clip), any-flag
     float *d_scratch = nullptr;    // render plans: float values [max_clips][S][F] before the uint8 map
     void *d_rparams = nullptr;     // render plans: WH_RENDER_PARAM_BYTES per clip

@@ -64,7 +64,6 @@ static constexpr int UM_PF = 2;     // converters prefetch windows this many uni
 static constexpr int UM_PCH = (36 + UM_CONV_WARPS - 1) / UM_CONV_WARPS;  // panel streaming: chunks per converter thread and panel
 static constexpr int UM_CONV_RC = 40 / UM_CONV_WARPS;  // register-prefetch converters: chunks per thread
 static constexpr int UM_WSLOTS = 4; // window buffers (panel streaming: panel slots; otherwise <= 2 used)
-static constexpr int UM_SEG = 8192; // panel streaming: samples per pre-pass max segment
 static constexpr int UM_SMEM_BUDGET = 227 * 1024 - 1024 - 256;
 // Accuracy bounds on the longest filter's half width (taps): the tensor core's fp32 accumulate
 // truncates, so the row error grows with the MMAs accumulated into one TMEM accumulator, about
@@ -109,8 +108,6 @@ struct UmmaArgs {
     int32_t acc2;                       // tf32: two accumulator sets per buffer (even / odd K-slices), added by the epilogue
     int32_t tma;                        // tf32: panels fetched by one TMA tensor copy each (tmap), else by cp.async
     int64_t full_end;                   // tma: samples of a clip covered by whole rows of V ((N / V) * V)
-    const float *segmax;                // pstream: max |x| per UM_SEG-sample segment [clips][nseg] (pre-pass)
-    int32_t nseg;
     const UmmaPass *passes;
     const UmmaTile *tiles;
     const UmmaGroup *groups;
@@ -825,7 +822,9 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
     __shared__ float xring[4];  // per-unit window exponent 2^-e, written by the converters
     __shared__ float red[UM_CONV_WARPS];
     __shared__ __align__(8) uint64_t stg_full, res_full, tab_full;
-    __shared__ __align__(8) uint64_t slot_full[UM_WSLOTS];  // tf32 panel streaming: a TMA panel copy has landed
+    __shared__ __align__(8) uint64_t slot_full[UM_WSLOTS];  // panel streaming: a TMA panel copy has landed
+    __shared__ __align__(8) uint64_t umax_full[4];          // panel streaming (fp16): a unit's window max is known
+    __shared__ uint32_t s_umax[4];                           // ... max |x| of the window (float bits), by unit % 4
     __shared__ uint32_t tmem_base_sh;
     __shared__ int s_decide;  // epilogue: CTA-uniform decision on the oldest pending unit
 
@@ -1007,6 +1006,7 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
         }
         mbar_init(&stg_full, 1);
         for (int i = 0; i < UM_WSLOTS; ++i) mbar_init(&slot_full[i], 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&umax_full[i], 1);
         mbar_init(&res_full, (CG == 2 && leader) ? 2 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1693,17 +1693,10 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 const int64_t own0 = tile * 128 * A.V, own1 = own0 + 128 * (int64_t)A.V;
                 uint32_t *rec = A.nfbad ? A.nfbad + b * (int64_t)(1 + WH_NF_CAP) : nullptr;
                 if (ct == 0) WH_TRACE(3, wcnt);
-                // the unit's exponent: max over the pre-pass segments its window touches
-                float mx = 0.0f;
-                {
-                    const int64_t lo = w0 > 0 ? w0 : 0, hi = w0 + (int64_t)A.win_rows * A.V;
-                    const int s0 = (int)(lo / UM_SEG);
-                    int s1 = (int)((hi - 1) / UM_SEG);
-                    if (s1 > A.nseg - 1) s1 = A.nseg - 1;
-                    for (int sg = s0 + lane; sg <= s1; sg += 32) mx = fmaxf(mx, __ldg(A.segmax + b * A.nseg + sg));
-#pragma unroll
-                    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-                }
+                // the unit's exponent: the window's max |x| (finite samples), scanned one unit ahead by
+                // the epilogue warps (whose loads also bring the window into L2 for the panel copies)
+                mbar_wait_p(&umax_full[wcnt & 3], (wcnt >> 2) & 1, pa, 2, pon);
+                const float mx = __uint_as_float(s_umax[wcnt & 3]);
                 const int ex = window_exponent(mx);
                 const float sc = ldexpf(1.0f, ex);
                 if (ct == 0) xring[wcnt & 3] = ldexpf(1.0f, -ex);
@@ -2114,10 +2107,72 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 --pend;
             }
         };
+        // Panel streaming (fp16): max |x| over the finite samples of a unit's window, one unit ahead
+        // of the converters (no pre-pass over the input; the loads allocate in L2, so the panel
+        // copies that follow read the window from there).  seq = the unit's position in this CTA's
+        // sequence; the result goes to s_umax[seq % 4], published through umax_full.
+        auto scan_window = [&](int64_t item, uint32_t seq) {
+            if (item >= n_units) return;
+            int64_t sb, stile;
+            unit_tile(item, sb, stile);
+            const int64_t w0 = stile * 128 * A.V - A.G0;
+            const int64_t lo = w0 > 0 ? w0 : 0;
+            int64_t hi = w0 + (int64_t)A.win_rows * A.V;
+            if (hi > A.N) hi = A.N;
+            const float *xb = A.x + sb * A.ld_x;
+            if (et == 0) s_umax[seq & 3] = 0u;
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * UM_EPI_WARPS) : "memory");
+            float mx = 0.0f;
+            if (A.vec_ok) {
+                const int64_t lo4 = (lo + 3) & ~(int64_t)3, hi4 = hi & ~(int64_t)3;
+                for (int64_t i = lo + et; i < lo4 && i < hi; i += 32 * UM_EPI_WARPS) {
+                    const float v = fabsf(__ldg(xb + i));
+                    mx = fmaxf(mx, v <= 3.402823466e38f ? v : 0.0f);
+                }
+                constexpr int64_t ST = 4 * 32 * UM_EPI_WARPS;  // samples per sweep of the epilogue threads
+                int64_t i = lo4 + 4 * (int64_t)et;
+                for (; i + 7 * ST + 4 <= hi4; i += 8 * ST) {  // eight independent loads in flight per thread
+                    float4 v[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float4 *>(xb + i + k * ST));
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float a0 = fabsf(v[k].x), a1 = fabsf(v[k].y), a2 = fabsf(v[k].z), a3 = fabsf(v[k].w);
+                        mx = fmaxf(mx, a0 <= 3.402823466e38f ? a0 : 0.0f);
+                        mx = fmaxf(mx, a1 <= 3.402823466e38f ? a1 : 0.0f);
+                        mx = fmaxf(mx, a2 <= 3.402823466e38f ? a2 : 0.0f);
+                        mx = fmaxf(mx, a3 <= 3.402823466e38f ? a3 : 0.0f);
+                    }
+                }
+                for (; i + 4 <= hi4; i += ST) {
+                    const float4 v = __ldg(reinterpret_cast<const float4 *>(xb + i));
+                    const float a0 = fabsf(v.x), a1 = fabsf(v.y), a2 = fabsf(v.z), a3 = fabsf(v.w);
+                    mx = fmaxf(mx, a0 <= 3.402823466e38f ? a0 : 0.0f);
+                    mx = fmaxf(mx, a1 <= 3.402823466e38f ? a1 : 0.0f);
+                    mx = fmaxf(mx, a2 <= 3.402823466e38f ? a2 : 0.0f);
+                    mx = fmaxf(mx, a3 <= 3.402823466e38f ? a3 : 0.0f);
+                }
+                for (int64_t i = (hi4 > lo4 ? hi4 : lo4) + et; i < hi; i += 32 * UM_EPI_WARPS) {
+                    const float v = fabsf(__ldg(xb + i));
+                    mx = fmaxf(mx, v <= 3.402823466e38f ? v : 0.0f);
+                }
+            } else {
+                for (int64_t i = lo + et; i < hi; i += 32 * UM_EPI_WARPS) {
+                    const float v = fabsf(__ldg(xb + i));
+                    mx = fmaxf(mx, v <= 3.402823466e38f ? v : 0.0f);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            if (lane == 0) atomicMax(&s_umax[seq & 3], __float_as_uint(mx));  // non-negative floats order as integers
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * UM_EPI_WARPS) : "memory");
+            if (et == 0) mbar_arrive(&umax_full[seq & 3]);
+        };
+        if (PS && !A.tf32) scan_window(u0, 0u);
         for (int64_t item = u0; item < n_units; item += ustride, ++ucnt) {
             int64_t b, tile;
             unit_tile(item, b, tile);
-            if (PS && et == 0) window_prefetch(item + 2 * ustride);  // L2, ahead of the panel copies
+            if (PS && !A.tf32) scan_window(item + ustride, ucnt + 1);
             const int64_t mrow = tile * 128 + m;  // global row (beyond rows_total: no frames)
             // first frame of this row (rs > 1: only every rs-th row is a frame)
             const int64_t frame0 = A.rs > 1 ? mrow / A.rs : mrow * P;
@@ -2240,33 +2295,6 @@ __global__ void __launch_bounds__(UM_THREADS, 1) k_umma(const __grid_constant__ 
                 A.nfctl[1] = 0u;
             }
         }
-    }
-}
-
-// ---- panel streaming: window exponents ------------------------------------------------
-// max |x| (finite samples) of each UM_SEG-sample segment of each clip; k_umma takes a unit's
-// exponent from the segments its window touches (a bound of the window's max: the split stays
-// exact to 2^-22 of it)
-__global__ void __launch_bounds__(256) k_seg_max(const float *__restrict__ x, int64_t ld_x, int64_t N, int32_t nseg,
-                                                 float *__restrict__ segmax) {
-    const int64_t b = blockIdx.y, s0 = (int64_t)blockIdx.x * UM_SEG;
-    const float *xb = x + b * ld_x;
-    int64_t s1 = s0 + UM_SEG;
-    if (s1 > N) s1 = N;
-    float mx = 0.0f;
-    for (int64_t i = s0 + threadIdx.x; i < s1; i += 256) {
-        const float v = __ldg(xb + i);
-        mx = fmaxf(mx, is_finite_f(v) ? fabsf(v) : 0.0f);
-    }
-    __shared__ float red[8];
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
-        mx = fmaxf(mx, red[0]);
-        segmax[b * nseg + blockIdx.x] = mx;
     }
 }
 
@@ -2598,9 +2626,8 @@ static int umma_prepare_impl(Plan &p) {
         // row a frame): the cheaper of the two by a model fitted to c4-shaped batches (cycles at
         // ~1.7 GHz; profiles/r02k_hops.txt): a unit (pair of 128-row tiles) costs its K-steps'
         // MMAs -- ~620 cycles per K-step panel-streamed, ~430 in rows of 128 -- or, panel-streamed,
-        // its panels' conversion (~30 cycles per window row and panel) if that is longer, plus the
-        // pre-pass over the input; units run in rounds over the CTA pairs.  Panel streaming must
-        // model 5 % cheaper to be taken.
+        // its panels' conversion (~30 cycles per window row and panel) if that is longer; units run
+        // in rounds over the CTA pairs.  Panel streaming must model 5 % cheaper to be taken.
         bool model_ps = false;
         if (H % 128 == 0 && H >= 256) {
             const double ksteps = (double)((2 * p.Lmax + 64) / 64 + 1);
@@ -2610,8 +2637,7 @@ static int umma_prepare_impl(Plan &p) {
             const double rounds_ps = std::ceil(clips * (double)((tiles_ps + 1) / 2) / pairs);
             const double rounds_128 = std::ceil(clips * (double)((tiles_128 + 1) / 2) / pairs);
             const double win_rows = 128.0 + (double)(2 * p.Lmax / H) + 8.0;
-            const double t_ps = rounds_ps * std::max(620.0 * ksteps, 30.0 * win_rows * (double)(H / 64)) +
-                                clips * (double)p.N * 1.05e-3;
+            const double t_ps = rounds_ps * std::max(620.0 * ksteps, 30.0 * win_rows * (double)(H / 64));
             const double t_128 = rounds_128 * 430.0 * ksteps;
             model_ps = t_ps < 0.95 * t_128;
         }
@@ -2783,10 +2809,13 @@ static int umma_prepare_impl(Plan &p) {
     {
         std::vector<UmmaPass> tp;
         std::vector<UmmaTile> tt;
-        const int64_t g0min = (p.Lmax + 31) / 32 * 32;
+        // (panel streaming with 64-sample fp16 panels: a multiple of 64, so that a panel never
+        // straddles two rows of V samples -- its TMA box is one rectangle of the batch tensor)
+        const int64_t gal = (p.pstream && !p.tf32) ? 64 : 32;
+        const int64_t g0min = (p.Lmax + gal - 1) / gal * gal;
         int64_t best = -1;
         double best_cost = 0.0;
-        for (int64_t g0 = g0min; g0 <= g0min + p.V; g0 += 32) {
+        for (int64_t g0 = g0min; g0 <= g0min + p.V; g0 += gal) {
             const double c = make_tiles(g0, tp, tt) * (g0 % p.V == 0 ? 1.0 : 1.03);
             if (best < 0 || c < best_cost - 0.5) {
                 best = g0;
@@ -3061,11 +3090,6 @@ static int umma_prepare_impl(Plan &p) {
     WH_CUDA_TRY(cudaMemcpy(p.d_groups_u, p.groups_u.data(), sizeof(UmmaGroup) * p.groups_u.size(),
                            cudaMemcpyHostToDevice));
     WH_CUDA_TRY(cudaMalloc(&p.d_bank, (size_t)p.bank_bytes));
-    if (p.pstream && !p.tf32) {
-        cudaFree(p.d_segmax);
-        p.d_segmax = nullptr;
-        WH_CUDA_TRY(cudaMalloc(&p.d_segmax, sizeof(float) * (size_t)p.max_clips * (size_t)((p.N + UM_SEG - 1) / UM_SEG)));
-    }
     WH_CUDA_TRY(cudaMalloc(&p.d_scale_pow, sizeof(float) * p.S));
     int32_t *d_fexp = nullptr;
     WH_CUDA_TRY(cudaMalloc(&d_fexp, sizeof(int32_t) * p.S));
@@ -3201,7 +3225,8 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     a.acc2 = p.acc2;
     a.full_end = (p.N / p.V) * p.V;
     a.tma = 0;
-    if (p.pstream && !p.no_tma && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && ld_x % 4 == 0 && p.N >= p.V &&
+    if (p.pstream && !p.no_tma && (p.tf32 || p.G0 % 64 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+        ld_x % 4 == 0 && p.N >= p.V &&
         p.win_rows <= 256 && clips <= 0x7fffffff && encode_tiled()) {
         // the batch as (V samples, N / V whole rows, clips): a window panel is one box of
         // 32 samples x win_rows rows; rows before / after the clip's whole rows are zero-filled
@@ -3218,8 +3243,6 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         a.tma = r == CUDA_SUCCESS ? 1 : 0;
     }
-    a.nseg = (int32_t)((p.N + UM_SEG - 1) / UM_SEG);
-    a.segmax = p.d_segmax;
     a.vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (ld_x % 4 == 0);
     a.tables = p.d_tables; a.tables_bytes = (uint32_t)p.tables_bytes;
     a.passes = p.d_passes; a.tiles = p.d_tiles; a.groups = p.d_groups_u; a.n_groups = (int32_t)p.groups_u.size(); a.bank = p.d_bank; a.scale_pow = p.d_scale_pow;
@@ -3256,12 +3279,6 @@ int umma_launch(Plan &p, const float *x, int64_t clips, int64_t ld_x, void *out,
     int64_t grid = std::min<int64_t>(units * p.cg, ctas);
     if (p.cg == 2) grid &= ~(int64_t)1;
     (void)cudaGetLastError();  // drop stale non-sticky errors of earlier runtime calls
-    if (p.pstream && !p.tf32) {
-        // the window exponents of panel streaming: max |x| per UM_SEG-sample segment
-        if (clips > 65535) return fail(WH_E_INVALID_ARG, "UMMA engine: too many clips for one launch");
-        k_seg_max<<<dim3((unsigned)a.nseg, (unsigned)clips), 256, 0, s>>>(x, ld_x, p.N, a.nseg, p.d_segmax);
-        WH_CUDA_TRY(cudaGetLastError());
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(UM_THREADS);
