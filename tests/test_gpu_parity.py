@@ -618,6 +618,25 @@ def test_very_long_taps():
     check_minmax(got, ref, O.cwth_batch(x, sc, 32, wavelet="rmor", output="abs"), "abs")
 
 
+@pytest.mark.parametrize("hop,n", [(640, 1000), (640, 3000), (320, 5000), (1024, 20000)])
+def test_panel_streaming_short_filters_and_short_clips(hop, n, monkeypatch):
+    """Panel streaming with filters much shorter than a row of hop samples and clips of a few
+    rows: the window origin falls inside a row, so a 64-sample panel must not straddle two
+    rows of the batch tensor the TMA copies read (the K origin is a multiple of 64), the
+    tensor has one or a few whole rows and the clip's partial last row comes from global memory."""
+    monkeypatch.setenv("WH_UMMA_PSTREAM", "1")
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, n)).astype(np.float32)
+    sc = np.geomspace(0.876, 51.487, 14)
+    for wavelet, output in (("cmor", "power"), ("rmor", "abs")):
+        plan = wh.CwthPlan(sc, None, hop, n, wavelet=wavelet, output=output, max_clips=2, engine="umma")
+        got = plan.execute_host(x)
+        plan.close()
+        ref = O.cwth_batch(x, sc, hop, wavelet=wavelet, output=output)
+        assert got.shape == ref.shape
+        assert row_rel_err(got, ref) <= (2e-5 if output == "power" else ROW_TOL), (hop, n, wavelet)
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
 def test_pass_groups_are_byte_identical(groups, monkeypatch):
     """Splitting a tile pair's passes into separate units (what the launcher does when there
