@@ -131,6 +131,7 @@ struct Plan {
     int32_t pstream = 0;           // UMMA: rows of hop samples (one frame each), window streamed by column panel
     bool no_pstream = false;       // UMMA planner retry without panel streaming
     int32_t tf32 = 0;              // UMMA panel streaming with kind::tf32 MMAs (no window exponent, no pre-pass)
+    bool ps_cg1 = false;           // panel streaming with single-CTA MMAs (a clip's last tile pair would be half empty)
     bool no_tma = false;           // planner override: tf32 panels fetched by cp.async instead of TMA tensor copies
     int32_t acc2 = 0;              // tf32: two accumulator sets per TMEM buffer (even / odd K-slices)
     int32_t ks = 64;               // taps per K-step: 64 (fp16 operands) or 32 (tf32 operands), 128 B per operand row

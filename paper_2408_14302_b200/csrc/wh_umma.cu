@@ -2629,17 +2629,23 @@ static int umma_prepare_impl(Plan &p) {
         // its panels' conversion (~30 cycles per window row and panel) if that is longer; units run
         // in rounds over the CTA pairs.  Panel streaming must model 5 % cheaper to be taken.
         bool model_ps = false;
-        if (H % 128 == 0 && H >= 256) {
+        p.ps_cg1 = false;
+        if (H % 64 == 0 && H >= 256) {
             const double ksteps = (double)((2 * p.Lmax + 64) / 64 + 1);
             const double pairs = std::max(1, p.sms / 2), clips = (double)std::max<int64_t>(1, p.max_clips);
             const int64_t tiles_ps = (p.F + 127) / 128, rows128 = (p.F - 1) * (H / 128) + 1;
             const int64_t tiles_128 = (rows128 + 127) / 128;
-            const double rounds_ps = std::ceil(clips * (double)((tiles_ps + 1) / 2) / pairs);
-            const double rounds_128 = std::ceil(clips * (double)((tiles_128 + 1) / 2) / pairs);
             const double win_rows = 128.0 + (double)(2 * p.Lmax / H) + 8.0;
-            const double t_ps = rounds_ps * std::max(620.0 * ksteps, 30.0 * win_rows * (double)(H / 64));
-            const double t_128 = rounds_128 * 430.0 * ksteps;
-            model_ps = t_ps < 0.95 * t_128;
+            const double unit_ps = std::max(620.0 * ksteps, 30.0 * win_rows * (double)(H / 64));
+            const double t_ps2 = std::ceil(clips * (double)((tiles_ps + 1) / 2) / pairs) * unit_ps;
+            // single-CTA MMAs (a unit = one tile) when a clip's last tile pair is half empty --
+            // clips of up to 128 frames at hop 1280: 120 vs 185 us on c4's shape
+            const double t_ps1 = std::ceil(clips * (double)tiles_ps / (2.0 * pairs)) * unit_ps;
+            p.ps_cg1 = t_ps1 < 0.9 * t_ps2;
+            if (H % 128 == 0) {
+                const double rounds_128 = std::ceil(clips * (double)((tiles_128 + 1) / 2) / pairs);
+                model_ps = std::min(t_ps1, t_ps2) < 0.95 * rounds_128 * 430.0 * ksteps;
+            }
         }
         const bool want = plan_knob("WH_UMMA_PSTREAM") != nullptr || H % 128 != 0 || model_ps;
         p.pstream = (!p.no_pstream && want && plan_knob("WH_UMMA_NO_PSTREAM") == nullptr && H >= 256 &&
@@ -2848,7 +2854,7 @@ static int umma_prepare_impl(Plan &p) {
     const int64_t win = 2LL * (p.pstream ? 1 : p.panels) * p.win_rows * 128;  // pstream: one panel slot
     int64_t byte_off = 0;
     // CTA pairs (tcgen05 cta_group::2, M = 256): each CTA stages half of every tap tile
-    p.cg = (p.sms % 2 == 0 && plan_knob("WH_UMMA_CG1") == nullptr) ? 2 : 1;
+    p.cg = (p.sms % 2 == 0 && plan_knob("WH_UMMA_CG1") == nullptr && !(p.pstream && p.ps_cg1)) ? 2 : 1;
     // Group consecutive tiles of a pass into one bulk copy of up to group_target bytes per
     // CTA: a copy costs ~250 issue cycles whatever its size (tools/probe_bulk.cu), so small
     // tiles must travel together.  Bank layout per group: [CTA-0 blocks][CTA-1 blocks].

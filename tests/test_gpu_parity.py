@@ -643,6 +643,28 @@ def test_panel_streaming_short_filters_and_short_clips(hop, n, monkeypatch):
         assert row_rel_err(got_u, ref) <= tol, (hop, n, wavelet, "unaligned")
 
 
+@pytest.mark.parametrize("hop", [1280, 1344, 2048])
+def test_panel_streaming_single_cta_units(hop):
+    """Many clips of at most 128 frames at a large hop: a CTA pair's second tile would be empty,
+    so the planner runs panel streaming with single-CTA MMAs (a unit = one 128-frame tile) --
+    against the oracle, a NaN clip included."""
+    n, clips = 24000, 200
+    x = synth.make_batch(4, clips=clips, n=n, start=3)
+    x[5, 7777] = np.nan
+    sc = synth.config_scales(4)[::2]
+    plan = wh.CwthPlan(sc, None, hop, n, wavelet="rmor", output="abs", max_clips=clips, engine="umma")
+    got = plan.execute_host(x)
+    plan.close()
+    keep = np.array([i for i in range(clips) if i != 5])
+    ref = O.cwth_batch(x[keep], sc, hop, wavelet="rmor", output="abs")
+    assert got.shape == (clips, len(sc), -(-n // hop))
+    assert row_rel_err(got[keep], ref) <= ROW_TOL
+    k = np.arange(got.shape[2])
+    for s_, a in enumerate(sc):
+        L = math.ceil(6.0 * a * math.sqrt(0.75))
+        np.testing.assert_array_equal(~np.isfinite(got[5, s_]), np.abs(k * hop - 7777) <= L)
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "8", "32"])
 def test_pass_groups_are_byte_identical(groups, monkeypatch):
     """Splitting a tile pair's passes into separate units (what the launcher does when there
